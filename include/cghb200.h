@@ -1,0 +1,219 @@
+/*
+ * cghb200 — C ABI of the B200-native hologram-generation hot path.
+ *
+ * Plain C types only (no torch, no CUDA types in signatures). Every entry
+ * point is reentrant: state lives in the caller's arguments or in an opaque
+ * plan owned by one thread at a time; each call/plan has its own CUDA stream.
+ * All host arrays are caller-owned, C-contiguous, row-major; complex arrays
+ * are interleaved (re, im) float64 — numpy complex128 layout.
+ *
+ * Each function names the reference interface it replaces
+ * (paths relative to /root/reference/pkg/src/cghkit/).
+ */
+#ifndef CGHB200_H
+#define CGHB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes: one per reference exception class (errors.py:79-108) --- */
+#define CGH_OK 0
+#define CGH_ERR_DIMENSION 1      /* DimensionMismatchError */
+#define CGH_ERR_ZERO_TARGET 2    /* ZeroTargetError */
+#define CGH_ERR_EMPTY_MASK 3     /* EmptyMaskError */
+#define CGH_ERR_INVALID_SPEC 4   /* InvalidSpecError */
+#define CGH_ERR_NONFINITE 5      /* NonFiniteError */
+#define CGH_ERR_ZERO_FIELD 6     /* ZeroFieldError */
+#define CGH_ERR_VALUE 7          /* ValueError (bad init mode / direction / argument) */
+#define CGH_ERR_UNSUPPORTED 8    /* shape outside the implemented set (raised loudly) */
+#define CGH_ERR_CUDA 9           /* CUDA runtime failure */
+#define CGH_ERR_NO_DEVICE 10     /* no CUDA device / library built without GPU */
+#define CGH_ERR_MEMORY 11        /* device or host allocation failed */
+
+#define CGH_FP32 0
+#define CGH_FP64 1
+
+#define CGH_SCHEME_PHASE 0       /* slm.py:18-31 PhaseOnly (binary_phase = 2 levels) */
+#define CGH_SCHEME_AMPLITUDE 1   /* slm.py:34-42 AmplitudeOnly */
+#define CGH_SCHEME_MULTI 2       /* slm.py:45-55 MultiAmp */
+
+#define CGH_FOURIER 0
+#define CGH_FRESNEL 1
+
+#define CGH_COMPLETED 0          /* algorithms.py:48-50 */
+#define CGH_CONVERGED 1
+#define CGH_CANCELLED 2
+
+#define CGH_INIT_RANDOM_PHASE 0  /* algorithms.py:42-43 */
+#define CGH_INIT_BACKPROPAGATE 1
+
+/* numpy PCG64 state (bit_generator.state): 128-bit state and increment, the
+ * buffered 32-bit half (has_uint32/uinteger). */
+typedef struct cgh_pcg64 {
+    uint64_t state_hi, state_lo;
+    uint64_t inc_hi, inc_lo;
+    int32_t has_uint32;
+    uint32_t uinteger;
+} cgh_pcg64;
+
+/* One generation problem: SLM (slm.py:58-64), scheme states (slm.py:71-79,
+ * computed by the caller exactly as the reference does), propagation
+ * (propagation.py:38-55) and metric flag (propagation.py:58-63). */
+typedef struct cgh_problem {
+    int32_t height, width;
+    int32_t precision;          /* CGH_FP32 | CGH_FP64 (GS/OSPR/transforms) */
+    int32_t device;
+    int32_t scheme_kind;
+    int32_t n_states;
+    double phase_offset;        /* PhaseOnly.phase_offset */
+    const double *states;       /* n_states complex128 */
+    int32_t prop_kind;          /* CGH_FOURIER | CGH_FRESNEL */
+    double wavelength, distance, pitch_x, pitch_y;
+    int32_t rescale;            /* MetricSpec.rescale */
+} cgh_problem;
+
+typedef int (*cgh_cancel_fn)(void *user);
+typedef void (*cgh_progress_fn)(void *user, int64_t k, double err);
+/* audit(k, incremental_unscaled_error, index_plane int32[H*W]) — SA/DBS test hook */
+typedef void (*cgh_audit_fn)(void *user, int64_t k, double inc_err, const int32_t *indices);
+
+typedef struct cgh_callbacks {
+    cgh_cancel_fn cancel;       /* polled before each iteration/frame/checkpoint chunk */
+    cgh_progress_fn progress;   /* called in order on the calling thread */
+    cgh_audit_fn audit;
+    void *user;
+} cgh_callbacks;
+
+/* RunReport (algorithms.py:84-94) minus the Python-side fields. The trace is
+ * written to caller arrays trace_k/trace_v of capacity trace_cap. */
+typedef struct cgh_report {
+    double final_error;
+    double efficiency;
+    int64_t iterations_executed;
+    int32_t termination;        /* CGH_COMPLETED | CGH_CONVERGED | CGH_CANCELLED */
+    int64_t trace_len;
+    int64_t kernel_launches;    /* kernels this call launched (evidence/bench) */
+    double device_ms;           /* CUDA-event time of the device work */
+} cgh_report;
+
+typedef struct cgh_gs_params {   /* algorithms.py:57-81 (gs fields) */
+    int32_t iterations;
+    double feedback_gain;
+    int32_t quantize_each_iteration;
+    int32_t init_mode;           /* CGH_INIT_* */
+    cgh_pcg64 rng;               /* PCG64(seed) — algorithms.py:160 */
+} cgh_gs_params;
+
+typedef struct cgh_ospr_params { /* algorithms.py:473-487 */
+    int32_t subframes;
+    const cgh_pcg64 *frame_rng;  /* subframes entries: PCG64(SeedSequence(seed).spawn(S)[i]) */
+} cgh_ospr_params;
+
+typedef struct cgh_sa_params {   /* algorithms.py:343-404 */
+    int64_t proposals;
+    double initial_temperature;  /* < 0 : auto (100 warm-up proposals) */
+    double cooling_factor;
+    int32_t init_mode;
+    cgh_pcg64 rng;               /* PCG64(seed) at draw 0 */
+    int64_t log_cap;             /* record the first log_cap proposals (0 = off) */
+    int64_t *log_pixel;          /* [log_cap] proposal pixel m*W+n (warm-up excluded) */
+    int32_t *log_level;          /* [log_cap] proposed level */
+    uint8_t *log_accept;         /* [log_cap] 1 = committed */
+} cgh_sa_params;
+
+typedef struct cgh_dbs_params {  /* algorithms.py:410-467 */
+    int32_t max_passes;
+    int32_t scan_random;         /* scan_order == "random" */
+    int32_t init_mode;
+    cgh_pcg64 rng;               /* PCG64(SeedSequence(seed)) at draw 0 */
+    /* random order: per-pass permutation streams PCG64(root.spawn(1)[0]),
+       one per pass (max_passes entries) — algorithms.py:437-439 */
+    const cgh_pcg64 *pass_rng;
+    int64_t log_cap;             /* record the first log_cap pixel visits */
+    int64_t *log_pixel;
+    int32_t *log_level;          /* committed level or -1 */
+    double *log_change;
+} cgh_dbs_params;
+
+/* ---- library ---------------------------------------------------------- */
+int cgh_version(void);
+const char *cgh_last_error(void);               /* thread-local message of the last failure */
+int cgh_device_count(int32_t *count);
+
+/* ---- transforms: propagation.py:81-94 (fft2), 110-123 (propagate[_inverse])
+ * op 0 = fft2 forward (centred), 1 = fft2 inverse, 2 = propagate,
+ * 3 = propagate_inverse. in/out: H*W complex128. Sizes: powers of two. */
+int cgh_transform(const cgh_problem *pb, const double *in, double *out, int32_t op);
+
+/* ---- masked metric sums on the device, fp64, fixed order (mse_error /
+ * efficiency, propagation.py:164-202). r = |replay|, t = |target|:
+ * out[6] = {count_in, sum_in t^2, sum_in r^2, sum_in r t, sum_in (scale r - t)^2, sum_all r^2}. */
+int cgh_masked_sums(int32_t device, const double *replay, const double *target, const uint8_t *mask,
+                    int64_t count, double scale, double *out);
+
+/* ---- slm.py:86-108 quantize_indices on the device (fp64). */
+int cgh_quantize(const cgh_problem *pb, const double *values, int64_t count, int32_t *out_idx);
+
+/* ---- runners. target: H*W complex128 (centred, as given to the reference);
+ * mask: H*W bytes (centred MetricSpec.mask); illumination: H*W complex128 or
+ * NULL. out_idx: index plane(s), uint8 when n_states <= 256 else int32.
+ * out_field (GS only, nullable): complex128 hologram after the last
+ * iteration's projection, before the final snap (parity checks). */
+int cgh_gs_run(const cgh_problem *pb, const cgh_gs_params *gp, const double *target, const uint8_t *mask,
+               const double *illumination, void *out_idx, double *out_field, int64_t *trace_k,
+               double *trace_v, int64_t trace_cap, cgh_report *rep, const cgh_callbacks *cb);   /* algorithms.py:147 run_gs */
+int cgh_ospr_run(const cgh_problem *pb, const cgh_ospr_params *op, const double *target, const uint8_t *mask,
+                 const double *illumination, void *out_idx, int64_t *trace_k, double *trace_v,
+                 int64_t trace_cap, cgh_report *rep, const cgh_callbacks *cb);                 /* algorithms.py:473 run_ospr */
+int cgh_sa_run(const cgh_problem *pb, const cgh_sa_params *sp, const double *target, const uint8_t *mask,
+               const double *illumination, void *out_idx, int64_t *trace_k, double *trace_v,
+               int64_t trace_cap, cgh_report *rep, const cgh_callbacks *cb);                   /* algorithms.py:343 run_sa */
+int cgh_dbs_run(const cgh_problem *pb, const cgh_dbs_params *dp, const double *target, const uint8_t *mask,
+                const double *illumination, void *out_idx, int64_t *trace_k, double *trace_v,
+                int64_t trace_cap, cgh_report *rep, const cgh_callbacks *cb);                  /* algorithms.py:410 run_dbs */
+
+/* ---- device-resident plans (benchmarks / batched callers) --------------
+ * A plan owns the device buffers and stream for one (H, W, precision, device).
+ * set_target uploads and prepares the target once; run_* then execute with
+ * inputs resident in HBM and leave the index planes on the device
+ * (cgh_plan_download_idx copies them out). */
+typedef struct cgh_plan cgh_plan;
+int cgh_plan_create(const cgh_problem *pb, cgh_plan **out);
+int cgh_plan_destroy(cgh_plan *plan);
+int cgh_plan_set_target(cgh_plan *plan, const double *target, const uint8_t *mask, const double *illumination);
+int cgh_plan_gs(cgh_plan *plan, const cgh_gs_params *gp, int64_t *trace_k, double *trace_v, int64_t trace_cap,
+                cgh_report *rep, const cgh_callbacks *cb);
+int cgh_plan_ospr(cgh_plan *plan, const cgh_ospr_params *op, int64_t *trace_k, double *trace_v,
+                  int64_t trace_cap, cgh_report *rep, const cgh_callbacks *cb);
+int cgh_plan_download_idx(cgh_plan *plan, void *out_idx, int64_t frames);
+void *cgh_plan_stream(cgh_plan *plan);          /* cudaStream_t of the plan */
+int cgh_plan_sync(cgh_plan *plan);
+
+/* ---- reference-kernel seam: kernels/__init__.py:42-44 (delta_error,
+ * commit_update, best_delta, _core.pyx:20-83) on the device, fp64.
+ * replay_m: count complex128 (in/out for commit); target_m: count float64;
+ * row_tw/col_tw: the pixel's DFT-table rows (complex128, lengths H and W). */
+int cgh_delta_error(int32_t device, const double *replay_m, const double *target_m, const double *row_tw,
+                    const double *col_tw, const int32_t *mu, const int32_t *mv, int64_t count, int32_t h,
+                    int32_t w, double delta_re, double delta_im, double *out);
+int cgh_commit_update(int32_t device, double *replay_m, const double *row_tw, const double *col_tw,
+                      const int32_t *mu, const int32_t *mv, int64_t count, int32_t h, int32_t w,
+                      double delta_re, double delta_im);
+int cgh_best_delta(int32_t device, const double *replay_m, const double *target_m, const double *row_tw,
+                   const double *col_tw, const int32_t *mu, const int32_t *mv, int64_t count, int32_t h,
+                   int32_t w, const double *deltas, int64_t levels, int64_t *best_index, double *best_change);
+
+/* ---- host-side numpy-stream emulation (no GPU needed) -----------------
+ * Generator.permutation(n) of a PCG64 stream (algorithms.py:437-439). */
+int cgh_permutation(const cgh_pcg64 *rng, int64_t n, int64_t *out);
+/* n doubles of Generator.random after skipping `skip` draws, on the device
+ * when device >= 0 (parity tests of the device emulation), else on the host. */
+int cgh_random_doubles(int32_t device, const cgh_pcg64 *rng, int64_t skip, int64_t n, double *out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CGHB200_H */

@@ -1,0 +1,202 @@
+"""ctypes binding of ``libcghb200.so`` (include/cghb200.h).
+
+The shared library is built in-tree (``__graft_entry__.build()`` /
+``make -C paper_2006_10509_b200/csrc``). There is no fallback: if the library
+or a CUDA device is missing, every compute entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+from . import errors
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libcghb200.so")
+
+OK = 0
+STATUS_NAMES = {
+    1: "DIMENSION", 2: "ZERO_TARGET", 3: "EMPTY_MASK", 4: "INVALID_SPEC", 5: "NONFINITE",
+    6: "ZERO_FIELD", 7: "VALUE", 8: "UNSUPPORTED", 9: "CUDA", 10: "NO_DEVICE", 11: "MEMORY",
+}
+FP32, FP64 = 0, 1
+SCHEME_PHASE, SCHEME_AMPLITUDE, SCHEME_MULTI = 0, 1, 2
+FOURIER, FRESNEL = 0, 1
+COMPLETED, CONVERGED, CANCELLED = 0, 1, 2
+INIT_RANDOM, INIT_BACKPROP = 0, 1
+
+# Every symbol include/cghb200.h declares (checked by tests/test_abi.py).
+EXPORTS = (
+    "cgh_version", "cgh_last_error", "cgh_device_count", "cgh_transform", "cgh_masked_sums", "cgh_quantize",
+    "cgh_gs_run", "cgh_ospr_run", "cgh_sa_run", "cgh_dbs_run",
+    "cgh_plan_create", "cgh_plan_destroy", "cgh_plan_set_target", "cgh_plan_gs", "cgh_plan_ospr",
+    "cgh_plan_download_idx", "cgh_plan_stream", "cgh_plan_sync",
+    "cgh_delta_error", "cgh_commit_update", "cgh_best_delta",
+    "cgh_permutation", "cgh_random_doubles",
+)
+
+
+class Pcg64State(ctypes.Structure):
+    _fields_ = [("state_hi", ctypes.c_uint64), ("state_lo", ctypes.c_uint64),
+                ("inc_hi", ctypes.c_uint64), ("inc_lo", ctypes.c_uint64),
+                ("has_uint32", ctypes.c_int32), ("uinteger", ctypes.c_uint32)]
+
+    @classmethod
+    def from_bitgen(cls, bitgen):
+        """From a numpy PCG64 bit generator's ``.state`` dict."""
+        st = bitgen.state
+        s, inc = st["state"]["state"], st["state"]["inc"]
+        m = (1 << 64) - 1
+        return cls(s >> 64, s & m, inc >> 64, inc & m, st["has_uint32"], st["uinteger"])
+
+
+class Problem(ctypes.Structure):
+    _fields_ = [("height", ctypes.c_int32), ("width", ctypes.c_int32), ("precision", ctypes.c_int32),
+                ("device", ctypes.c_int32), ("scheme_kind", ctypes.c_int32), ("n_states", ctypes.c_int32),
+                ("phase_offset", ctypes.c_double), ("states", ctypes.c_void_p), ("prop_kind", ctypes.c_int32),
+                ("wavelength", ctypes.c_double), ("distance", ctypes.c_double), ("pitch_x", ctypes.c_double),
+                ("pitch_y", ctypes.c_double), ("rescale", ctypes.c_int32)]
+
+
+CANCEL_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p)
+PROGRESS_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_int64, ctypes.c_double)
+AUDIT_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_int64, ctypes.c_double, ctypes.POINTER(ctypes.c_int32))
+
+
+class Callbacks(ctypes.Structure):
+    _fields_ = [("cancel", CANCEL_FN), ("progress", PROGRESS_FN), ("audit", AUDIT_FN), ("user", ctypes.c_void_p)]
+
+
+class Report(ctypes.Structure):
+    _fields_ = [("final_error", ctypes.c_double), ("efficiency", ctypes.c_double),
+                ("iterations_executed", ctypes.c_int64), ("termination", ctypes.c_int32),
+                ("trace_len", ctypes.c_int64), ("kernel_launches", ctypes.c_int64), ("device_ms", ctypes.c_double)]
+
+
+class GsParams(ctypes.Structure):
+    _fields_ = [("iterations", ctypes.c_int32), ("feedback_gain", ctypes.c_double),
+                ("quantize_each_iteration", ctypes.c_int32), ("init_mode", ctypes.c_int32), ("rng", Pcg64State)]
+
+
+class OsprParams(ctypes.Structure):
+    _fields_ = [("subframes", ctypes.c_int32), ("frame_rng", ctypes.POINTER(Pcg64State))]
+
+
+class SaParams(ctypes.Structure):
+    _fields_ = [("proposals", ctypes.c_int64), ("initial_temperature", ctypes.c_double),
+                ("cooling_factor", ctypes.c_double), ("init_mode", ctypes.c_int32), ("rng", Pcg64State),
+                ("log_cap", ctypes.c_int64), ("log_pixel", ctypes.POINTER(ctypes.c_int64)),
+                ("log_level", ctypes.POINTER(ctypes.c_int32)), ("log_accept", ctypes.POINTER(ctypes.c_uint8))]
+
+
+class DbsParams(ctypes.Structure):
+    _fields_ = [("max_passes", ctypes.c_int32), ("scan_random", ctypes.c_int32), ("init_mode", ctypes.c_int32),
+                ("rng", Pcg64State), ("pass_rng", ctypes.POINTER(Pcg64State)), ("log_cap", ctypes.c_int64),
+                ("log_pixel", ctypes.POINTER(ctypes.c_int64)), ("log_level", ctypes.POINTER(ctypes.c_int32)),
+                ("log_change", ctypes.POINTER(ctypes.c_double))]
+
+
+_lib = None
+_lock = threading.Lock()
+
+
+def library(required=True):
+    """Load the shared library once (raises if missing and ``required``)."""
+    global _lib
+    if _lib is None:
+        with _lock:
+            if _lib is None:
+                if not os.path.exists(LIB_PATH):
+                    if not required:
+                        return None
+                    raise errors.BackendUnavailableError(
+                        f"{LIB_PATH} is not built; run __graft_entry__.build() "
+                        "(make -C paper_2006_10509_b200/csrc)")
+                lib = ctypes.CDLL(LIB_PATH)
+                _declare(lib)
+                _lib = lib
+    return _lib
+
+
+def _declare(lib):
+    P = ctypes.c_void_p
+    i32, i64, f64 = ctypes.c_int32, ctypes.c_int64, ctypes.c_double
+    pP = ctypes.POINTER
+    sig = {
+        "cgh_version": ([], ctypes.c_int),
+        "cgh_last_error": ([], ctypes.c_char_p),
+        "cgh_device_count": ([pP(i32)], ctypes.c_int),
+        "cgh_transform": ([pP(Problem), P, P, i32], ctypes.c_int),
+        "cgh_quantize": ([pP(Problem), P, i64, P], ctypes.c_int),
+        "cgh_masked_sums": ([i32, P, P, P, i64, f64, P], ctypes.c_int),
+        "cgh_gs_run": ([pP(Problem), pP(GsParams), P, P, P, P, P, P, P, i64, pP(Report), pP(Callbacks)], ctypes.c_int),
+        "cgh_ospr_run": ([pP(Problem), pP(OsprParams), P, P, P, P, P, P, i64, pP(Report), pP(Callbacks)], ctypes.c_int),
+        "cgh_sa_run": ([pP(Problem), pP(SaParams), P, P, P, P, P, P, i64, pP(Report), pP(Callbacks)], ctypes.c_int),
+        "cgh_dbs_run": ([pP(Problem), pP(DbsParams), P, P, P, P, P, P, i64, pP(Report), pP(Callbacks)], ctypes.c_int),
+        "cgh_plan_create": ([pP(Problem), pP(P)], ctypes.c_int),
+        "cgh_plan_destroy": ([P], ctypes.c_int),
+        "cgh_plan_set_target": ([P, P, P, P], ctypes.c_int),
+        "cgh_plan_gs": ([P, pP(GsParams), P, P, i64, pP(Report), pP(Callbacks)], ctypes.c_int),
+        "cgh_plan_ospr": ([P, pP(OsprParams), P, P, i64, pP(Report), pP(Callbacks)], ctypes.c_int),
+        "cgh_plan_download_idx": ([P, P, i64], ctypes.c_int),
+        "cgh_plan_stream": ([P], P),
+        "cgh_plan_sync": ([P], ctypes.c_int),
+        "cgh_delta_error": ([i32, P, P, P, P, P, P, i64, i32, i32, f64, f64, pP(f64)], ctypes.c_int),
+        "cgh_commit_update": ([i32, P, P, P, P, P, i64, i32, i32, f64, f64], ctypes.c_int),
+        "cgh_best_delta": ([i32, P, P, P, P, P, P, i64, i32, i32, P, i64, pP(i64), pP(f64)], ctypes.c_int),
+        "cgh_permutation": ([pP(Pcg64State), i64, P], ctypes.c_int),
+        "cgh_random_doubles": ([i32, pP(Pcg64State), i64, i64, P], ctypes.c_int),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+
+
+def last_error():
+    return (library().cgh_last_error() or b"").decode("utf-8", "replace")
+
+
+def check(status):
+    """Map a C status to the reference's exception classes (errors.py:79-108)."""
+    if status == OK:
+        return
+    msg = last_error()
+    exc = {
+        1: errors.DimensionMismatchError,
+        2: errors.ZeroTargetError,
+        3: errors.EmptyMaskError,
+        4: errors.InvalidSpecError,
+        5: errors.NonFiniteError,
+        6: errors.ZeroFieldError,
+        7: ValueError,
+        8: errors.UnsupportedShapeError,
+        9: errors.DeviceError,
+        10: errors.BackendUnavailableError,
+        11: MemoryError,
+    }.get(status, errors.DeviceError)
+    raise exc(msg)
+
+
+def ptr(a):
+    return None if a is None else ctypes.c_void_p(a.ctypes.data)
+
+
+def device_count():
+    n = ctypes.c_int32(0)
+    st = library().cgh_device_count(ctypes.byref(n))
+    return int(n.value) if st == OK else 0
+
+
+def require_device():
+    if device_count() == 0:
+        raise errors.BackendUnavailableError(
+            "no CUDA device visible: the B200 path has no CPU fallback (" + last_error() + ")")
+
+
+def c128(a):
+    return np.ascontiguousarray(a, dtype=np.complex128)

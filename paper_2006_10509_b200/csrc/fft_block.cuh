@@ -1,0 +1,192 @@
+// Register/shared-memory FFT of one line (row or column) of N points.
+//
+// Layout contract ("strided-natural"): the TF = N/E threads that own a line
+// each hold E elements, thread t holding v[r] = x[t + r*TF]. run_fft()
+// consumes and produces that layout, so a forward transform can feed an
+// inverse transform register-to-register (the replay-plane projection of GS
+// sits between them) and global loads/stores are unit stride across t.
+//
+// Algorithm: Stockham auto-sort, radix E (E in {2,4,8,16}) per stage with a
+// smaller final radix when log2(N) is not a multiple of log2(E). Butterflies
+// are fully unrolled with compile-time roots of unity; inter-stage twiddles
+// come from an N-entry table tw[k] = exp(-2 pi i k / N) built in fp64 on the
+// host (conjugated for the inverse). Stages exchange through shared memory
+// stored as split re/im arrays with one pad word per 128 bytes.
+#pragma once
+#include "cx.cuh"
+
+namespace cgh {
+
+// ---------------------------------------------------------------- radix DFTs
+// In-place DFT of R points v[0], v[S], ..., v[(R-1)S]; natural-order output.
+template <int R, int DIR, int S, class T>
+struct Dft;
+
+template <int DIR, int S, class T>
+struct Dft<1, DIR, S, T> {
+    __device__ __forceinline__ static void run(cx<T>*) {}
+};
+
+template <int DIR, int S, class T>
+struct Dft<2, DIR, S, T> {
+    __device__ __forceinline__ static void run(cx<T>* v) {
+        cx<T> a = v[0], b = v[S];
+        v[0] = a + b;
+        v[S] = a - b;
+    }
+};
+
+template <int DIR, int S, class T>
+struct Dft<4, DIR, S, T> {
+    __device__ __forceinline__ static void run(cx<T>* v) {
+        cx<T> a = v[0] + v[2 * S], b = v[0] - v[2 * S];
+        cx<T> c = v[S] + v[3 * S], d = rot90<DIR>(v[S] - v[3 * S]);
+        v[0] = a + c;
+        v[2 * S] = a - c;
+        v[S] = b + d;
+        v[3 * S] = b - d;
+    }
+};
+
+// R = R1 * R2 split ("four-step in registers"): n = R2*n1 + n2, k = k1 + R1*k2.
+template <int R1, int R2, int DIR, int S, class T>
+struct DftSplit {
+    template <int N2>
+    __device__ __forceinline__ static void inner(cx<T>* v) {
+        if constexpr (N2 < R2) {
+            Dft<R1, DIR, S * R2, T>::run(v + S * N2);   // over n1, stride R2
+            twiddle<N2, 1>(v);
+            inner<N2 + 1>(v);
+        }
+    }
+    template <int N2, int K1>
+    __device__ __forceinline__ static void twiddle(cx<T>* v) {
+        if constexpr (K1 < R1) {
+            v[S * (N2 + R2 * K1)] = mul_root<T, DIR, long(N2) * K1, long(R1) * R2>(v[S * (N2 + R2 * K1)]);
+            twiddle<N2, K1 + 1>(v);
+        }
+    }
+    template <int K1>
+    __device__ __forceinline__ static void outer(cx<T>* v) {
+        if constexpr (K1 < R1) {
+            Dft<R2, DIR, S, T>::run(v + S * R2 * K1);   // over n2, contiguous block
+            outer<K1 + 1>(v);
+        }
+    }
+    __device__ __forceinline__ static void run(cx<T>* v) {
+        inner<0>(v);
+        outer<0>(v);
+        // element (k1, k2) now at index R2*k1 + k2; natural index k1 + R1*k2
+        cx<T> tmp[R1 * R2];
+#pragma unroll
+        for (int i = 0; i < R1 * R2; ++i) tmp[i] = v[S * i];
+#pragma unroll
+        for (int k1 = 0; k1 < R1; ++k1)
+#pragma unroll
+            for (int k2 = 0; k2 < R2; ++k2) v[S * (k1 + R1 * k2)] = tmp[R2 * k1 + k2];
+    }
+};
+
+template <int DIR, int S, class T>
+struct Dft<8, DIR, S, T> {
+    __device__ __forceinline__ static void run(cx<T>* v) { DftSplit<2, 4, DIR, S, T>::run(v); }
+};
+template <int DIR, int S, class T>
+struct Dft<16, DIR, S, T> {
+    __device__ __forceinline__ static void run(cx<T>* v) { DftSplit<4, 4, DIR, S, T>::run(v); }
+};
+template <int DIR, int S, class T>
+struct Dft<32, DIR, S, T> {
+    __device__ __forceinline__ static void run(cx<T>* v) { DftSplit<4, 8, DIR, S, T>::run(v); }
+};
+
+// --------------------------------------------------------------- line FFT
+__host__ __device__ constexpr int ilog2(int n) { return n <= 1 ? 0 : 1 + ilog2(n / 2); }
+
+// Elements per thread for a line of N points at precision T.
+template <class T, int N>
+struct LineShape {
+    static constexpr int EMAX = sizeof(T) == 8 ? 8 : 16;
+    static constexpr int E = N < EMAX ? N : EMAX;
+    static constexpr int TF = N / E;   // threads per line
+};
+
+// Shared-memory words per line (split re/im, padded).
+template <class T>
+__host__ __device__ constexpr int pad_unit() { return 128 / int(sizeof(T)); }
+template <class T>
+__device__ __forceinline__ int padx(int i) { return i + i / pad_unit<T>(); }
+template <class T, int N>
+__host__ __device__ constexpr int line_words() { return N + N / pad_unit<T>() + 1; }
+
+template <class T, int N, int DIR>
+struct LineFft {
+    using Sh = LineShape<T, N>;
+    static constexpr int E = Sh::E;
+    static constexpr int TF = Sh::TF;
+
+    template <int NS>
+    __device__ __forceinline__ static void stages(cx<T> (&v)[E], T* sre, T* sim, int t, const cx<T>* __restrict__ tw) {
+        constexpr int R = (N / NS >= E) ? E : N / NS;
+        constexpr int NB = E / R;
+        // v[b*R + r] = x_s[j + r*N/R], j = t + b*TF
+        if constexpr (NS > 1) {
+#pragma unroll
+            for (int b = 0; b < NB; ++b) {
+                const int j = t + b * TF;
+                const int jm = j & (NS - 1);
+#pragma unroll
+                for (int r = 1; r < R; ++r) {
+                    cx<T> w = ldg_cx(tw + jm * r * (N / (NS * R)));
+                    v[b * R + r] = DIR < 0 ? cmul(v[b * R + r], w) : cmulc(v[b * R + r], w);
+                }
+            }
+        }
+#pragma unroll
+        for (int b = 0; b < NB; ++b) Dft<R, DIR, 1, T>::run(&v[b * R]);
+
+        if constexpr (NS * R == N) {
+            // last stage: output X[t + b*TF + r*N/R] = strided index (b + r*NB)
+            if constexpr (NB > 1) {
+                cx<T> tmp[E];
+#pragma unroll
+                for (int i = 0; i < E; ++i) tmp[i] = v[i];
+#pragma unroll
+                for (int b = 0; b < NB; ++b)
+#pragma unroll
+                    for (int r = 0; r < R; ++r) v[b + r * NB] = tmp[b * R + r];
+            }
+        } else {
+            __syncthreads();
+#pragma unroll
+            for (int b = 0; b < NB; ++b) {
+                const int j = t + b * TF;
+                const int base = (j / NS) * NS * R + (j & (NS - 1));
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const int p = padx<T>(base + r * NS);
+                    sre[p] = v[b * R + r].x;
+                    sim[p] = v[b * R + r].y;
+                }
+            }
+            __syncthreads();
+            constexpr int R2 = (N / (NS * R) >= E) ? E : N / (NS * R);
+            constexpr int NB2 = E / R2;
+#pragma unroll
+            for (int b = 0; b < NB2; ++b)
+#pragma unroll
+                for (int r = 0; r < R2; ++r) {
+                    const int p = padx<T>(t + b * TF + r * (N / R2));
+                    v[b * R2 + r] = mk(sre[p], sim[p]);
+                }
+            stages<NS * R>(v, sre, sim, t, tw);
+        }
+    }
+
+    // Transform one line held in strided-natural layout (unscaled).
+    __device__ __forceinline__ static void run(cx<T> (&v)[E], T* sre, T* sim, int t, const cx<T>* __restrict__ tw) {
+        stages<1>(v, sre, sim, t, tw);
+    }
+};
+
+}  // namespace cgh

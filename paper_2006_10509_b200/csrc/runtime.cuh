@@ -1,0 +1,133 @@
+// Host runtime shared by the C-ABI translation units: plans, buffers, errors.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/cghb200.h"
+#include "dispatch.cuh"
+
+namespace cgh {
+
+// ----------------------------------------------------------------- errors
+void set_error(const char* fmt, ...);
+int fail(int code, const char* fmt, ...);
+
+#define CGH_CUDA(call)                                                                      \
+    do {                                                                                    \
+        cudaError_t e_ = (call);                                                            \
+        if (e_ != cudaSuccess)                                                              \
+            return ::cgh::fail(e_ == cudaErrorMemoryAllocation ? CGH_ERR_MEMORY : CGH_ERR_CUDA, \
+                               "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__); \
+    } while (0)
+
+#define CGH_TRY(call)            \
+    do {                         \
+        int s_ = (call);         \
+        if (s_ != CGH_OK) return s_; \
+    } while (0)
+
+inline Pcg64 to_pcg(const cgh_pcg64& g) {
+    Pcg64 r;
+    r.state = (u128(g.state_hi) << 64) | u128(g.state_lo);
+    r.inc = (u128(g.inc_hi) << 64) | u128(g.inc_lo);
+    r.has_uint32 = g.has_uint32;
+    r.uinteger = g.uinteger;
+    return r;
+}
+
+inline bool is_pow2(int n) { return n >= 2 && (n & (n - 1)) == 0; }
+
+// ------------------------------------------------------------------ plan
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+};
+
+}  // namespace cgh
+
+struct cgh_plan {
+    int dev = 0, H = 0, W = 0, prec = 0;
+    cudaStream_t st = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    std::vector<cudaEvent_t> evpool;
+    // scheme / propagation / metric
+    int scheme_kind = 0, nstates = 0;
+    double offset = 0, step = 0;
+    int prop_kind = 0;
+    double wl = 0, dist = 0, px = 0, py = 0;
+    int rescale = 0;
+    // device buffers
+    cgh::DevBuf states64, states32, tw_row, tw_col, q_row, q_col;
+    cgh::DevBuf data, tgt, beam, idx, field, partials, counter, stats, stage, mask, frame_rng, intensity;
+    cgh::DevBuf sa_buf;   // search state (SA/DBS)
+    int idx_bytes = 1;
+    bool has_beam = false, target_ready = false;
+    // mapped host results
+    double* res_h = nullptr;
+    double* res_d = nullptr;
+    size_t res_cap = 0;
+    // prep statistics
+    double count_in = 0, denom = 0, nf_in = 0, nf_all = 0, nf_beam = 0;
+    long launches = 0;
+    int idx_frames = 0;   // index planes currently held
+};
+
+namespace cgh {
+
+int plan_init(cgh_plan* P, const cgh_problem* pb);
+void plan_free(cgh_plan* P);
+int ensure(cgh_plan* P, DevBuf& b, size_t bytes);
+int ensure_res(cgh_plan* P, size_t n);
+int ensure_events(cgh_plan* P, size_t n);
+int plan_upload_target(cgh_plan* P, const double* target, const uint8_t* mask, const double* illum);
+
+template <class T>
+PassArgs<T> base_args(cgh_plan* P);
+
+template <class T>
+inline int run_row(cgh_plan* P, int mode, const PassArgs<T>& a, int frames) {
+    cudaError_t e = launch_row<T>(mode, P->W, a, frames, P->st);
+    P->launches += 1;
+    if (e != cudaSuccess) return fail(CGH_ERR_CUDA, "row pass (mode %d, W=%d): %s", mode, P->W, cudaGetErrorString(e));
+    return CGH_OK;
+}
+template <class T>
+inline int run_col(cgh_plan* P, int mode, const PassArgs<T>& a, int frames) {
+    cudaError_t e = launch_col<T>(mode, P->H, a, frames, P->st);
+    P->launches += 1;
+    if (e != cudaSuccess) return fail(CGH_ERR_CUDA, "column pass (mode %d, H=%d): %s", mode, P->H, cudaGetErrorString(e));
+    return CGH_OK;
+}
+
+inline int grid_for(long total) {
+    long g = (total + 255) / 256;
+    if (g > 148 * 16) g = 148 * 16;
+    if (g < 1) g = 1;
+    return int(g);
+}
+
+// In-order progress delivery with a bounded number of iterations in flight:
+// after each enqueue, completed entries are reported; if more than `depth`
+// are pending the oldest is waited for (the GPU keeps the rest queued).
+struct ProgressQueue {
+    cgh_plan* P = nullptr;
+    const cgh_callbacks* cb = nullptr;
+    size_t depth = 64;
+    const double* values = nullptr;   // mapped host results
+    long stride = 1;                  // values[k * stride] is entry k
+    long kbias = 0;                   // progress(k + kbias, ...)
+    std::vector<long> ks;
+    std::vector<cudaEvent_t> evs;
+    size_t head = 0, used = 0;
+    int init(cgh_plan* P_, const cgh_callbacks* cb_, size_t depth_, const double* values_, long stride_);
+    int push(long k);
+    int poll(bool all);
+};
+
+}  // namespace cgh
