@@ -1,0 +1,373 @@
+#!/usr/bin/env python3
+"""Benchmark of the hologram-generation hot path (BASELINE.json metric).
+
+Headline workload (configs[2], C3): Fresnel Gerchberg-Saxton, 2048x2048,
+PhaseOnly(8) quantisation, 200 iterations, full-plane mask, synthetic target
+(SURVEY.md §8d). One step = one complete GS run (start field, 200 fused
+iterations, final snap + replay error/efficiency) with the target already
+resident in HBM. value = GS iterations/s summed over all ranks.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 runs under torchrun, one process per GPU; each rank generates its own
+hologram (seed 1 + rank): replicas, weak scaling, no data-path collective
+(the path does not shard below one hologram at this size).
+
+Extra objects on the JSON line: e2e (same metric through the drop-in
+``run_gs`` with host numpy buffers), roofline (dominant pass, live CUDA-event
+timing vs MEASURED_PEAKS.json), cpu_baseline (the oracle port on this host),
+clocks (nvidia-smi sampled during the timed region), ospr (C2 holograms/s).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+import numpy as np  # noqa: E402
+
+N_PX = 2048
+ITERS = 200
+LEVELS = 8
+GS_BYTES_PER_PX = 36          # complex64: row pass 8+8, column pass 8+8+4
+COL_BYTES_PER_PX = 20
+ROW_BYTES_PER_PX = 16
+OSPR_N = 1024
+OSPR_S = 24
+METRIC = "GS iterations/s (Fresnel 2048x2048, PhaseOnly(8), 200 iterations per run)"
+
+
+def peaks():
+    path = os.path.join(REPO, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:  # noqa: BLE001
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def make_cfg(seed, n=N_PX, levels=LEVELS, kind="fresnel", algorithm="gs", iterations=ITERS, subframes=8):
+    from paper_2006_10509_b200 import algorithms as A
+    from paper_2006_10509_b200.image import rect_mask
+    from paper_2006_10509_b200.propagation import MetricSpec, PropagationSpec
+    from paper_2006_10509_b200.slm import PhaseOnly, SlmSpec
+
+    return A.AlgorithmConfig(algorithm=algorithm, slm=SlmSpec(n, n, PhaseOnly(levels)),
+                             propagation=PropagationSpec(kind), metric=MetricSpec(rect_mask(n, n), rescale=False),
+                             seed=seed, iterations=iterations, subframes=subframes)
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 200 ms (B200_PROFILING.md)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:  # noqa: BLE001
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.out = ""
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except Exception:  # noqa: BLE001
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        for line in (getattr(self, "out", "") or "").strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 6:
+                rows.append(parts)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": float(rows[0][1]),
+                "reasons": reasons, "samples": len(rows)}
+
+
+def cpu_baseline_gs(seconds_hint=20):
+    """Oracle port (numpy, 1 core) on a bounded sample of the C3 workload:
+    steady-state iterations/s from progress timestamps of a short run."""
+    from oracle import cgh_oracle
+    from paper_2006_10509_b200.workloads import natural_target
+
+    m = 6
+    cfg = make_cfg(1, iterations=m)
+    target = natural_target(N_PX)
+    stamps = []
+    t0 = time.perf_counter()
+    cgh_oracle.gs(cfg, target, progress=lambda k, e: stamps.append((k, time.perf_counter())))
+    wall = time.perf_counter() - t0
+    loop = [s for s in stamps if s[0] < m]
+    rate = (loop[-1][0] - loop[0][0]) / (loop[-1][1] - loop[0][1])
+    return {"value": rate, "unit": "iter/s", "cores": 1, "kind": "port",
+            "sample": f"oracle/cgh_oracle.gs (numpy restatement of run_gs) at 2048^2 Fresnel PhaseOnly(8), "
+                      f"{m} iterations, steady-state rate from progress timestamps (run wall {wall:.1f}s)"}
+
+
+def run_reference(args):
+    """--impl reference: the reference's CPU algorithm (oracle port) on all host
+    cores: one independent C3 run per core (numpy releases the GIL), each step
+    a bounded sample of 3 loop iterations per replica."""
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import cgh_oracle
+    from paper_2006_10509_b200.workloads import natural_target
+
+    try:
+        cores = len(os.sched_getaffinity(0))
+    except Exception:  # noqa: BLE001
+        cores = os.cpu_count() or 1
+    m = 4
+    target = natural_target(N_PX)
+
+    def one(seed):
+        stamps = []
+        cgh_oracle.gs(make_cfg(seed, iterations=m), target,
+                      progress=lambda k, e: stamps.append((k, time.perf_counter())))
+        loop = [s for s in stamps if s[0] < m]
+        return loop[-1][0] - loop[0][0], loop[0][1], loop[-1][1]
+
+    def step(pool, s):
+        res = list(pool.map(one, [1 + s * cores + i for i in range(cores)]))
+        iters = sum(r[0] for r in res)
+        span = max(r[2] for r in res) - min(r[1] for r in res)
+        return iters, span
+
+    with ThreadPoolExecutor(max_workers=cores) as pool:
+        for w in range(args.warmup):
+            step(pool, -1 - w)
+        tot_i, tot_t = 0, 0.0
+        for s in range(args.steps):
+            i, t = step(pool, s)
+            tot_i += i
+            tot_t += t
+    value = tot_i / tot_t
+    sample = (f"oracle port of run_gs on {cores} host threads, one C3 replica per thread, "
+              f"{m - 1} loop iterations per replica per step (init/final excluded)")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "iter/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * tot_t / max(1, args.steps),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "C3: Fresnel GS 2048x2048 PhaseOnly(8), 200 it (bounded sample)",
+                       "parallelism": f"{cores} CPU threads"},
+            "cpu_baseline": {"value": value, "unit": "iter/s", "cores": cores, "kind": "port", "sample": sample},
+            "e2e": {"value": value, "unit": "iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    world, rank, local = dist_env()
+    import torch
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.SUM)
+        return float(t.item())
+
+    from paper_2006_10509_b200 import _native
+    from paper_2006_10509_b200 import algorithms as A
+    from paper_2006_10509_b200.plan import GenerationPlan
+    from paper_2006_10509_b200.runtime import device, precision
+    from paper_2006_10509_b200.workloads import natural_target
+
+    seed = 1 + rank
+    cfg = make_cfg(seed)
+    target = natural_target(N_PX)
+    plan = GenerationPlan(cfg, (N_PX, N_PX), precision=_native.FP32, device=local)
+    plan.set_target(target)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")   # > 126 MB L2
+
+    for _ in range(args.warmup):
+        plan.gs(seed=seed)
+    step_ms = []
+    launches = 0
+    barrier()
+    with ClockSampler(local) as clk:
+        t_wall = time.perf_counter()
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            rep, _ = plan.gs(seed=seed)      # device_ms: CUDA events on the plan's stream
+            step_ms.append(rep.device_ms)
+            launches += rep.kernel_launches
+        barrier()
+        t_wall = time.perf_counter() - t_wall
+    total_ms = max_over_ranks(sum(step_ms))
+    value = world * args.steps * ITERS / (total_ms / 1000.0)
+    launches = int(sum_over_ranks(launches))
+
+    # per-pass timing (live CUDA events around each launch) for the roofline
+    plan.profile(True)
+    flush.zero_()
+    torch.cuda.synchronize()
+    plan.gs(seed=seed)
+    passes = plan.profile(False)
+    hw = N_PX * N_PX
+    peak, peak_src = peaks()
+    cand = []
+    for name, bpp in (("col_gs", COL_BYTES_PER_PX), ("row_holo", ROW_BYTES_PER_PX)):
+        ms, cnt = passes.get(name, (0.0, 0))
+        if cnt:
+            avg = ms / cnt
+            cand.append((ms, name, bpp * hw / (avg / 1000.0) / 1e9, avg, bpp))
+    cand.sort(reverse=True)
+    traffic = None
+    tpath = os.path.join(REPO, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(cand[0][1]) if cand else None
+        except Exception:  # noqa: BLE001
+            traffic = None
+    iter_ms = (sum(step_ms) / len(step_ms)) / ITERS
+    roofline = None
+    if cand:
+        _, name, achieved, avg_ms, bpp = cand[0]
+        roofline = {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                    "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                    "algorithmic_bytes_per_launch": bpp * hw, "avg_launch_ms": avg_ms,
+                    "per_iteration": {"bytes": GS_BYTES_PER_PX * hw, "ms": iter_ms,
+                                      "achieved": GS_BYTES_PER_PX * hw / (iter_ms / 1000.0) / 1e9,
+                                      "frac": GS_BYTES_PER_PX * hw / (iter_ms / 1000.0) / 1e9 / peak},
+                    "passes_ms": {k: v[0] / max(1, v[1]) for k, v in passes.items()}}
+
+    # e2e: the drop-in run_gs with host numpy buffers (H2D target+mask, D2H indices)
+    e2e = None
+    if not args.no_e2e:
+        with device(local), precision("fp32"):
+            A.run_gs(cfg, target)       # warm
+            barrier()
+            t0 = time.perf_counter()
+            ke = max(1, min(args.steps, 3))
+            for _ in range(ke):
+                A.run_gs(cfg, target)
+            barrier()
+            te = max_over_ranks(time.perf_counter() - t0)
+        e2e = {"value": world * ke * ITERS / te, "unit": "iter/s",
+               "h2d_bytes_per_step": hw * 16 + hw, "d2h_bytes_per_step": hw * 1 + (ITERS + 1) * 16,
+               "note": "run_gs(cfg, numpy complex128 target) per step: pageable H2D of target+mask, "
+                       "D2H of the uint8 index plane, host states[idx] expansion"}
+
+    # OSPR, C2 (1024^2 binary, 24 subframes): holograms/s, resident target
+    ospr = None
+    if not args.no_ospr:
+        from paper_2006_10509_b200.slm import binary_phase, SlmSpec
+
+        ocfg = make_cfg(seed, n=OSPR_N, kind="fourier", algorithm="ospr", subframes=OSPR_S)
+        ocfg.slm = SlmSpec(OSPR_N, OSPR_N, binary_phase())
+        oplan = GenerationPlan(ocfg, (OSPR_N, OSPR_N), precision=_native.FP32, device=local)
+        oplan.set_target(natural_target(OSPR_N))
+        for _ in range(max(1, args.warmup)):
+            oplan.ospr(seed=seed)
+        barrier()
+        oms = []
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            r, _ = oplan.ospr(seed=seed)
+            oms.append(r.device_ms)
+        otot = max_over_ranks(sum(oms))
+        ohw = OSPR_N * OSPR_N
+        obytes = (33 * OSPR_S + 8) * ohw
+        avg = sum(oms) / len(oms)
+        ospr = {"metric": "OSPR holograms/s (1024x1024 binary, 24 subframes)",
+                "value": world * args.steps / (otot / 1000.0), "unit": "holograms/s", "ms_per_hologram": avg,
+                "roofline": {"bound": "hbm", "achieved": obytes / (avg / 1000.0) / 1e9, "peak": peak, "unit": "GB/s",
+                             "frac": obytes / (avg / 1000.0) / 1e9 / peak, "algorithmic_bytes": obytes}}
+        oplan.close()
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline_gs()
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "iter/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": {"workload": "C3: Fresnel GS 2048x2048, PhaseOnly(8), 200 iterations per run, "
+                                       "full-plane mask, natural_target, seed 1+rank",
+                           "global_batch": world, "parallelism": f"replicas x{world}",
+                           "l2": "256 MB device write between timed steps (excluded from step time)"},
+                "gpu_launches": launches, "wall_s_timed": t_wall,
+                "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clk.summary(), "ospr": ospr}
+        print(json.dumps(line), flush=True)
+    plan.close()
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-ospr", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

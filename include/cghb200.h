@@ -190,6 +190,10 @@ int cgh_plan_ospr(cgh_plan *plan, const cgh_ospr_params *op, int64_t *trace_k, d
                   int64_t trace_cap, cgh_report *rep, const cgh_callbacks *cb);
 int cgh_plan_download_idx(cgh_plan *plan, void *out_idx, int64_t frames);
 void *cgh_plan_stream(cgh_plan *plan);          /* cudaStream_t of the plan */
+/* Per-pass CUDA-event timing: returns the accumulated ms / launch counts per
+ * pass id since the last call (ids: row modes 0-7, column modes 8-15, search
+ * kernels 16-23; n entries), clears them, and switches timing on/off. */
+int cgh_plan_profile(cgh_plan *plan, int32_t enable, double *ms, int64_t *counts, int32_t n);
 int cgh_plan_sync(cgh_plan *plan);
 
 /* ---- reference-kernel seam: kernels/__init__.py:42-44 (delta_error,

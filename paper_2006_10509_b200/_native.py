@@ -34,7 +34,7 @@ EXPORTS = (
     "cgh_version", "cgh_last_error", "cgh_device_count", "cgh_transform", "cgh_masked_sums", "cgh_quantize",
     "cgh_gs_run", "cgh_ospr_run", "cgh_sa_run", "cgh_dbs_run",
     "cgh_plan_create", "cgh_plan_destroy", "cgh_plan_set_target", "cgh_plan_gs", "cgh_plan_ospr",
-    "cgh_plan_download_idx", "cgh_plan_stream", "cgh_plan_sync",
+    "cgh_plan_download_idx", "cgh_plan_stream", "cgh_plan_sync", "cgh_plan_profile",
     "cgh_delta_error", "cgh_commit_update", "cgh_best_delta",
     "cgh_permutation", "cgh_random_doubles",
 )
@@ -145,6 +145,7 @@ def _declare(lib):
         "cgh_plan_download_idx": ([P, P, i64], ctypes.c_int),
         "cgh_plan_stream": ([P], P),
         "cgh_plan_sync": ([P], ctypes.c_int),
+        "cgh_plan_profile": ([P, i32, P, P, i32], ctypes.c_int),
         "cgh_delta_error": ([i32, P, P, P, P, P, P, i64, i32, i32, f64, f64, pP(f64)], ctypes.c_int),
         "cgh_commit_update": ([i32, P, P, P, P, P, i64, i32, i32, f64, f64], ctypes.c_int),
         "cgh_best_delta": ([i32, P, P, P, P, P, P, i64, i32, i32, P, i64, pP(i64), pP(f64)], ctypes.c_int),

@@ -273,6 +273,15 @@ int plan_upload_target(cgh_plan* P, const double* target, const uint8_t* mask, c
     return P->prec == CGH_FP64 ? prep_target<double>(P, target, mask, illum) : prep_target<float>(P, target, mask, illum);
 }
 
+int prof_mark(cgh_plan* P, int id, bool start) {
+    cudaEvent_t e;
+    CGH_CUDA(cudaEventCreate(&e));
+    CGH_CUDA(cudaEventRecord(e, P->st));
+    P->prof_ev.push_back(e);
+    if (start) P->prof_id.push_back(id);
+    return CGH_OK;
+}
+
 // ========================================================= progress queue
 int ProgressQueue::init(cgh_plan* P_, const cgh_callbacks* cb_, size_t depth_, const double* values_, long stride_) {
     P = P_;
@@ -721,6 +730,32 @@ int cgh_plan_download_idx(cgh_plan* plan, void* out_idx, int64_t frames) {
     const size_t bytes = size_t(frames) * plan->H * plan->W * plan->idx_bytes;
     if (bytes) CGH_CUDA(cudaMemcpyAsync(out_idx, plan->idx.p, bytes, cudaMemcpyDeviceToHost, plan->st));
     CGH_CUDA(cudaStreamSynchronize(plan->st));
+    return CGH_OK;
+}
+
+int cgh_plan_profile(cgh_plan* plan, int32_t enable, double* ms, int64_t* counts, int32_t n) {
+    if (!plan) return fail(CGH_ERR_VALUE, "null plan");
+    CGH_CUDA(cudaSetDevice(plan->dev));
+    if (ms && counts) {
+        CGH_CUDA(cudaStreamSynchronize(plan->st));
+        for (int i = 0; i < n; ++i) {
+            ms[i] = 0;
+            counts[i] = 0;
+        }
+        for (size_t k = 0; k < plan->prof_id.size() && 2 * k + 1 < plan->prof_ev.size(); ++k) {
+            float t = 0;
+            CGH_CUDA(cudaEventElapsedTime(&t, plan->prof_ev[2 * k], plan->prof_ev[2 * k + 1]));
+            const int id = plan->prof_id[k];
+            if (id >= 0 && id < n) {
+                ms[id] += t;
+                counts[id] += 1;
+            }
+        }
+    }
+    for (auto e : plan->prof_ev) cudaEventDestroy(e);
+    plan->prof_ev.clear();
+    plan->prof_id.clear();
+    plan->profiling = enable != 0;
     return CGH_OK;
 }
 

@@ -75,6 +75,10 @@ struct cgh_plan {
     // prep statistics
     double count_in = 0, denom = 0, nf_in = 0, nf_all = 0, nf_beam = 0;
     long launches = 0;
+    // per-pass CUDA-event timing (cgh_plan_profile): (pass id, start, end)
+    bool profiling = false;
+    std::vector<int> prof_id;
+    std::vector<cudaEvent_t> prof_ev;
     int idx_frames = 0;   // index planes currently held
 };
 
@@ -90,16 +94,24 @@ int plan_upload_target(cgh_plan* P, const double* target, const uint8_t* mask, c
 template <class T>
 PassArgs<T> base_args(cgh_plan* P);
 
+// Record a timing event before (start) / after a pass launch. Pass ids:
+// row modes 0..7, column modes 8 + mode, search kernels 16+.
+int prof_mark(cgh_plan* P, int id, bool start);
+
 template <class T>
 inline int run_row(cgh_plan* P, int mode, const PassArgs<T>& a, int frames) {
+    if (P->profiling) CGH_TRY(prof_mark(P, mode, true));
     cudaError_t e = launch_row<T>(mode, P->W, a, frames, P->st);
+    if (P->profiling) CGH_TRY(prof_mark(P, mode, false));
     P->launches += 1;
     if (e != cudaSuccess) return fail(CGH_ERR_CUDA, "row pass (mode %d, W=%d): %s", mode, P->W, cudaGetErrorString(e));
     return CGH_OK;
 }
 template <class T>
 inline int run_col(cgh_plan* P, int mode, const PassArgs<T>& a, int frames) {
+    if (P->profiling) CGH_TRY(prof_mark(P, 8 + mode, true));
     cudaError_t e = launch_col<T>(mode, P->H, a, frames, P->st);
+    if (P->profiling) CGH_TRY(prof_mark(P, 8 + mode, false));
     P->launches += 1;
     if (e != cudaSuccess) return fail(CGH_ERR_CUDA, "column pass (mode %d, H=%d): %s", mode, P->H, cudaGetErrorString(e));
     return CGH_OK;

@@ -1,0 +1,103 @@
+"""Device-resident generation plans (``cgh_plan_*``): the target stays in HBM
+across runs, index planes stay on the device until downloaded. Used by the
+batched / multi-GPU layer and by bench.py for the inputs-resident timing."""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _native
+from .algorithms import _init_code, _mask_bytes
+from .propagation import fill_propagation
+from .runtime import current_device, runner_precision
+from .slm import problem_for
+
+# pass ids reported by cgh_plan_profile
+PASS_NAMES = {0: "row_fwd", 1: "row_inv", 2: "row_holo", 3: "row_init", 4: "ospr_gen", 5: "ospr_acc",
+              8: "col_fwd", 9: "col_inv", 10: "col_gs", 11: "col_final", 12: "col_holo"}
+
+
+class GenerationPlan:
+    def __init__(self, cfg, shape, precision=None, device=None):
+        self.lib = _native.library()
+        _native.require_device()
+        h, w = shape
+        prec = runner_precision() if precision is None else precision
+        dev = current_device() if device is None else device
+        self.pb, self._keep = problem_for(cfg.slm.scheme, h, w, prec, dev)
+        fill_propagation(self.pb, cfg.propagation)
+        self.pb.rescale = 1 if cfg.metric.rescale else 0
+        self.cfg = cfg
+        self.shape = (h, w)
+        self.handle = ctypes.c_void_p()
+        _native.check(self.lib.cgh_plan_create(ctypes.byref(self.pb), ctypes.byref(self.handle)))
+        self.idx_dtype = np.uint8 if self.pb.n_states <= 256 else np.int32
+
+    def close(self):
+        if self.handle:
+            self.lib.cgh_plan_destroy(self.handle)
+            self.handle = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+    def set_target(self, target, illumination=None):
+        target = _native.c128(target)
+        mask = _mask_bytes(self.cfg, target)
+        ill = None if illumination is None else _native.c128(illumination)
+        _native.check(self.lib.cgh_plan_set_target(self.handle, _native.ptr(target), _native.ptr(mask),
+                                                   _native.ptr(ill)))
+
+    def gs(self, seed=None, iterations=None, with_trace=True):
+        cfg = self.cfg
+        gp = _native.GsParams()
+        gp.iterations = int(cfg.iterations if iterations is None else iterations)
+        gp.feedback_gain = float(cfg.feedback_gain)
+        gp.quantize_each_iteration = 1 if cfg.quantize_each_iteration else 0
+        gp.init_mode = _init_code(cfg.init_mode)
+        gp.rng = _native.Pcg64State.from_bitgen(np.random.PCG64(cfg.seed if seed is None else seed))
+        rep = _native.Report()
+        cap = gp.iterations + 1
+        tk = np.zeros(cap, np.int64) if with_trace else None
+        tv = np.zeros(cap, np.float64) if with_trace else None
+        _native.check(self.lib.cgh_plan_gs(self.handle, ctypes.byref(gp), _native.ptr(tk), _native.ptr(tv),
+                                           cap if with_trace else 0, ctypes.byref(rep), None))
+        return rep, (tk, tv)
+
+    def ospr(self, seed=None, subframes=None):
+        cfg = self.cfg
+        nsub = int(cfg.subframes if subframes is None else subframes)
+        streams = np.random.SeedSequence(cfg.seed if seed is None else seed).spawn(nsub)
+        fr = (_native.Pcg64State * max(1, nsub))()
+        for i, s in enumerate(streams):
+            fr[i] = _native.Pcg64State.from_bitgen(np.random.PCG64(s))
+        op = _native.OsprParams(nsub, ctypes.cast(fr, ctypes.POINTER(_native.Pcg64State)))
+        rep = _native.Report()
+        tk = np.zeros(max(1, nsub), np.int64)
+        tv = np.zeros(max(1, nsub), np.float64)
+        _native.check(self.lib.cgh_plan_ospr(self.handle, ctypes.byref(op), _native.ptr(tk), _native.ptr(tv),
+                                             max(1, nsub), ctypes.byref(rep), None))
+        return rep, (tk, tv)
+
+    def download_indices(self, frames=1):
+        out = np.empty((frames,) + self.shape, self.idx_dtype)
+        _native.check(self.lib.cgh_plan_download_idx(self.handle, _native.ptr(out), frames))
+        return out
+
+    def stream(self):
+        return self.lib.cgh_plan_stream(self.handle)
+
+    def sync(self):
+        _native.check(self.lib.cgh_plan_sync(self.handle))
+
+    def profile(self, enable):
+        """Switch per-pass event timing; returns {pass: (ms_total, launches)} since the last call."""
+        ms = np.zeros(24, np.float64)
+        cnt = np.zeros(24, np.int64)
+        _native.check(self.lib.cgh_plan_profile(self.handle, 1 if enable else 0, _native.ptr(ms), _native.ptr(cnt), 24))
+        return {PASS_NAMES.get(i, f"pass{i}"): (float(ms[i]), int(cnt[i])) for i in range(24) if cnt[i]}
