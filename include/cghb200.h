@@ -188,6 +188,10 @@ int cgh_plan_gs(cgh_plan *plan, const cgh_gs_params *gp, int64_t *trace_k, doubl
                 cgh_report *rep, const cgh_callbacks *cb);
 int cgh_plan_ospr(cgh_plan *plan, const cgh_ospr_params *op, int64_t *trace_k, double *trace_v,
                   int64_t trace_cap, cgh_report *rep, const cgh_callbacks *cb);
+int cgh_plan_sa(cgh_plan *plan, const cgh_sa_params *sp, int64_t *trace_k, double *trace_v, int64_t trace_cap,
+                cgh_report *rep, const cgh_callbacks *cb);      /* plan must be CGH_FP64 */
+int cgh_plan_dbs(cgh_plan *plan, const cgh_dbs_params *dp, int64_t *trace_k, double *trace_v, int64_t trace_cap,
+                 cgh_report *rep, const cgh_callbacks *cb);     /* plan must be CGH_FP64 */
 int cgh_plan_download_idx(cgh_plan *plan, void *out_idx, int64_t frames);
 void *cgh_plan_stream(cgh_plan *plan);          /* cudaStream_t of the plan */
 /* Per-pass CUDA-event timing: returns the accumulated ms / launch counts per

@@ -34,6 +34,7 @@ EXPORTS = (
     "cgh_version", "cgh_last_error", "cgh_device_count", "cgh_transform", "cgh_masked_sums", "cgh_quantize",
     "cgh_gs_run", "cgh_ospr_run", "cgh_sa_run", "cgh_dbs_run",
     "cgh_plan_create", "cgh_plan_destroy", "cgh_plan_set_target", "cgh_plan_gs", "cgh_plan_ospr",
+    "cgh_plan_sa", "cgh_plan_dbs",
     "cgh_plan_download_idx", "cgh_plan_stream", "cgh_plan_sync", "cgh_plan_profile",
     "cgh_delta_error", "cgh_commit_update", "cgh_best_delta",
     "cgh_permutation", "cgh_random_doubles",
@@ -143,6 +144,8 @@ def _declare(lib):
         "cgh_plan_gs": ([P, pP(GsParams), P, P, i64, pP(Report), pP(Callbacks)], ctypes.c_int),
         "cgh_plan_ospr": ([P, pP(OsprParams), P, P, i64, pP(Report), pP(Callbacks)], ctypes.c_int),
         "cgh_plan_download_idx": ([P, P, i64], ctypes.c_int),
+        "cgh_plan_sa": ([P, pP(SaParams), P, P, i64, pP(Report), pP(Callbacks)], ctypes.c_int),
+        "cgh_plan_dbs": ([P, pP(DbsParams), P, P, i64, pP(Report), pP(Callbacks)], ctypes.c_int),
         "cgh_plan_stream": ([P], P),
         "cgh_plan_sync": ([P], ctypes.c_int),
         "cgh_plan_profile": ([P, i32, P, P, i32], ctypes.c_int),

@@ -326,7 +326,6 @@ int ProgressQueue::poll(bool all) {
     return CGH_OK;
 }
 
-static bool cancelled(const cgh_callbacks* cb) { return cb && cb->cancel && cb->cancel(cb->user); }
 
 // ============================================================= transforms
 template <class T>

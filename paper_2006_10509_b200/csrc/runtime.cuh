@@ -117,6 +117,8 @@ inline int run_col(cgh_plan* P, int mode, const PassArgs<T>& a, int frames) {
     return CGH_OK;
 }
 
+inline bool cancelled(const cgh_callbacks* cb) { return cb && cb->cancel && cb->cancel(cb->user); }
+
 inline int grid_for(long total) {
     long g = (total + 255) / 256;
     if (g > 148 * 16) g = 148 * 16;
