@@ -218,10 +218,10 @@ def run_gs(cfg, target, illumination=None, progress=None, cancel=None):
     target = np.asarray(target, dtype=np.complex128)
     _check_inputs(cfg, target, illumination)
     init = _init_code(cfg.init_mode)
-    lib = _native.library()
-    _native.require_device()
     pb, keep = _problem(cfg, target)
     mask = _mask_bytes(cfg, target)
+    lib = _native.library()
+    _native.require_device()
     tgt = _native.c128(target)
     ill = _illum(illumination)
     gp = _native.GsParams()
@@ -258,10 +258,10 @@ def gs_field(cfg, target, illumination=None):
     """Parity helper: (index plane, pre-snap hologram field, report) of run_gs."""
     target = np.asarray(target, dtype=np.complex128)
     _check_inputs(cfg, target, illumination)
-    lib = _native.library()
-    _native.require_device()
     pb, keep = _problem(cfg, target)
     mask = _mask_bytes(cfg, target)
+    lib = _native.library()
+    _native.require_device()
     tgt = _native.c128(target)
     ill = _illum(illumination)
     gp = _native.GsParams(int(cfg.iterations), float(cfg.feedback_gain), 1 if cfg.quantize_each_iteration else 0,
@@ -287,10 +287,10 @@ def run_ospr(cfg, target, illumination=None, progress=None, cancel=None):
     start = time.perf_counter()
     target = np.asarray(target, dtype=np.complex128)
     _check_inputs(cfg, target, illumination)
-    lib = _native.library()
-    _native.require_device()
     pb, keep = _problem(cfg, target)
     mask = _mask_bytes(cfg, target)
+    lib = _native.library()
+    _native.require_device()
     tgt = _native.c128(target)
     ill = _illum(illumination)
     nsub = max(0, int(cfg.subframes))

@@ -31,10 +31,11 @@ def _prep(cfg, target, illumination):
     target = np.asarray(target, dtype=np.complex128)
     _check_inputs(cfg, target, illumination)
     init = _init_code(cfg.init_mode)
-    lib = _native.library()
-    _native.require_device()
     pb, keep = _problem(cfg, target)
     pb.precision = _native.FP64
+    _mask_bytes(cfg, target)
+    lib = _native.library()
+    _native.require_device()
     return target, init, lib, pb, keep
 
 
