@@ -1,0 +1,197 @@
+// Host side of the pipelined complex64 GS passes (fast_passes.cuh).
+#include <cudaTypedefs.h>
+
+#include "fast_passes.cuh"
+#include "runtime.cuh"
+
+namespace cgh {
+
+struct FastState {
+    CUtensorMap tmap;           // data as float32 [H][2W], box {2C, 256}
+    const void* tmap_ptr = nullptr;
+    int H = 0, W = 0;
+    DevBuf tgt_tiled, ctr;
+    const void* tgt_src = nullptr;
+};
+
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+template <int N>
+static int lines_of() {
+    return FastShape<N>::LINES;
+}
+
+static int fast_lines(int n) {
+    switch (n) {
+        case 256: return lines_of<256>();
+        case 512: return lines_of<512>();
+        case 1024: return lines_of<1024>();
+        case 2048: return lines_of<2048>();
+        case 4096: return lines_of<4096>();
+        default: return 0;
+    }
+}
+
+bool fast_eligible(cgh_plan* P) {
+    if (P->prec != CGH_FP32) return false;
+    const int lr = fast_lines(P->W), lc = fast_lines(P->H);
+    if (!lr || !lc) return false;
+    if (P->H < lr || P->W < lc) return false;
+    if (getenv("CGHB200_NO_FAST")) return false;
+    return encode_fn() != nullptr;
+}
+
+void fast_free(cgh_plan* P) {
+    FastState* F = static_cast<FastState*>(P->fast);
+    if (!F) return;
+    if (F->tgt_tiled.p) cudaFreeAsync(F->tgt_tiled.p, P->st);
+    if (F->ctr.p) cudaFreeAsync(F->ctr.p, P->st);
+    delete F;
+    P->fast = nullptr;
+}
+
+// Tensor map over the data buffer, tiled target, tile counters.
+int fast_prepare(cgh_plan* P) {
+    FastState* F = static_cast<FastState*>(P->fast);
+    if (!F) {
+        F = new FastState();
+        P->fast = F;
+    }
+    const int C = fast_lines(P->H);
+    if (F->tmap_ptr != P->data.p || F->H != P->H || F->W != P->W) {
+        cuuint64_t dims[2] = {cuuint64_t(2) * P->W, cuuint64_t(P->H)};
+        cuuint64_t strides[1] = {cuuint64_t(P->W) * 8};
+        cuuint32_t box[2] = {cuuint32_t(2 * C), cuuint32_t(std::min(kFastBoxRows, P->H))};
+        cuuint32_t estr[2] = {1, 1};
+        CUresult r = encode_fn()(&F->tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, P->data.p, dims, strides, box, estr,
+                                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return fail(CGH_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", int(r));
+        F->tmap_ptr = P->data.p;
+        F->H = P->H;
+        F->W = P->W;
+    }
+    if (!F->ctr.p) {
+        CGH_TRY(ensure(P, F->ctr, 64));
+        CGH_CUDA(cudaMemsetAsync(F->ctr.p, 0, 64, P->st));
+    }
+    if (F->tgt_src != P->tgt.p || !F->tgt_tiled.p) {
+        const long long n = (long long)P->H * P->W;
+        CGH_TRY(ensure(P, F->tgt_tiled, size_t(n) * 4));
+        tile_target_kernel<<<grid_for(n), 256, 0, P->st>>>(static_cast<const float*>(P->tgt.p),
+                                                          static_cast<float*>(F->tgt_tiled.p), P->H, P->W, C);
+        P->launches += 1;
+        CGH_CUDA(cudaGetLastError());
+        F->tgt_src = P->tgt.p;
+    }
+    return CGH_OK;
+}
+
+void fast_invalidate_target(cgh_plan* P) {
+    FastState* F = static_cast<FastState*>(P->fast);
+    if (F) F->tgt_src = nullptr;
+}
+
+static FastArgs fast_args(cgh_plan* P, const PassArgs<float>& a) {
+    FastState* F = static_cast<FastState*>(P->fast);
+    FastArgs f;
+    f.data = reinterpret_cast<float2*>(a.data);
+    f.H = P->H;
+    f.W = P->W;
+    f.beam = a.beam;
+    f.tw_row = a.tw_row;
+    f.tw_col = a.tw_col;
+    f.q_row = a.q_row;
+    f.q_col = a.q_col;
+    f.tgt_tiled = static_cast<const float*>(F->tgt_tiled.p);
+    f.gain = a.gain;
+    f.scale = a.scale;
+    f.tile_ctr = static_cast<unsigned*>(F->ctr.p);
+    f.red = a.red;
+    return f;
+}
+
+static int sm_count(int dev) {
+    static int cached[64] = {0};
+    if (!cached[dev & 63]) cudaDeviceGetAttribute(&cached[dev & 63], cudaDevAttrMultiProcessorCount, dev);
+    return cached[dev & 63];
+}
+
+template <int N>
+static cudaError_t row_launch(cgh_plan* P, const FastArgs& f) {
+    using S = FastShape<N>;
+    const size_t smem = size_t(2) * FastSlots<N>::ROW * sizeof(float2);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(fast_row_holo<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        attr = true;
+    }
+    const int tiles = P->H / S::LINES;
+    const int grid = std::max(1, std::min(sm_count(P->dev), tiles));
+    fast_row_holo<N><<<grid, kFastThreads, smem, P->st>>>(f);
+    return cudaGetLastError();
+}
+
+template <int N>
+static cudaError_t col_launch(cgh_plan* P, const FastArgs& f) {
+    using S = FastShape<N>;
+    FastState* F = static_cast<FastState*>(P->fast);
+    const size_t smem = size_t(2) * FastSlots<N>::COL * sizeof(float2);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(fast_col_gs<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        attr = true;
+    }
+    const int tiles = P->W / S::LINES;
+    const int grid = std::max(1, std::min(sm_count(P->dev), tiles));
+    fast_col_gs<N><<<grid, kFastThreads, smem, P->st>>>(f, F->tmap);
+    return cudaGetLastError();
+}
+
+int fast_row(cgh_plan* P, const PassArgs<float>& a) {
+    const FastArgs f = fast_args(P, a);
+    if (P->profiling) CGH_TRY(prof_mark(P, ROW_HOLO, true));
+    cudaError_t e;
+    switch (P->W) {
+        case 256: e = row_launch<256>(P, f); break;
+        case 512: e = row_launch<512>(P, f); break;
+        case 1024: e = row_launch<1024>(P, f); break;
+        case 2048: e = row_launch<2048>(P, f); break;
+        case 4096: e = row_launch<4096>(P, f); break;
+        default: return fail(CGH_ERR_UNSUPPORTED, "fast row pass W=%d", P->W);
+    }
+    if (P->profiling) CGH_TRY(prof_mark(P, ROW_HOLO, false));
+    P->launches += 1;
+    if (e != cudaSuccess) return fail(CGH_ERR_CUDA, "fast row pass: %s", cudaGetErrorString(e));
+    return CGH_OK;
+}
+
+int fast_col(cgh_plan* P, const PassArgs<float>& a) {
+    const FastArgs f = fast_args(P, a);
+    if (P->profiling) CGH_TRY(prof_mark(P, 8 + COL_GS, true));
+    cudaError_t e;
+    switch (P->H) {
+        case 256: e = col_launch<256>(P, f); break;
+        case 512: e = col_launch<512>(P, f); break;
+        case 1024: e = col_launch<1024>(P, f); break;
+        case 2048: e = col_launch<2048>(P, f); break;
+        case 4096: e = col_launch<4096>(P, f); break;
+        default: return fail(CGH_ERR_UNSUPPORTED, "fast column pass H=%d", P->H);
+    }
+    if (P->profiling) CGH_TRY(prof_mark(P, 8 + COL_GS, false));
+    P->launches += 1;
+    if (e != cudaSuccess) return fail(CGH_ERR_CUDA, "fast column pass: %s", cudaGetErrorString(e));
+    return CGH_OK;
+}
+
+}  // namespace cgh

@@ -182,6 +182,7 @@ void plan_free(cgh_plan* P) {
     if (!P) return;
     cudaSetDevice(P->dev);
     if (P->st) cudaStreamSynchronize(P->st);
+    fast_free(P);
     cgh::DevBuf* bufs[] = {&P->states64, &P->states32, &P->tw_row, &P->tw_col, &P->q_row, &P->q_col, &P->data,
                            &P->tgt, &P->beam, &P->idx, &P->field, &P->partials, &P->counter, &P->stats, &P->stage,
                            &P->mask, &P->frame_rng, &P->intensity, &P->sa_buf};
@@ -264,6 +265,7 @@ static int prep_target(cgh_plan* P, const double* target, const uint8_t* mask, c
     P->nf_all = st[3];
     P->nf_beam = st[4];
     P->target_ready = true;
+    fast_invalidate_target(P);
     return CGH_OK;
 }
 
@@ -406,6 +408,11 @@ static int gs_exec(cgh_plan* P, const cgh_gs_params* gp, int64_t* tk, double* tv
         return run_row<T>(P, ROW_HOLO, b, 1);
     };
 
+    bool fast = false;
+    if constexpr (sizeof(T) == 4) {
+        fast = fast_eligible(P);
+        if (fast) CGH_TRY(fast_prepare(P));
+    }
     CGH_TRY(run_init(iters == 0 ? 1 : 0));
     ProgressQueue pq;
     const bool has_cancel = cb && cb->cancel, has_progress = cb && cb->progress;
@@ -419,14 +426,26 @@ static int gs_exec(cgh_plan* P, const cgh_gs_params* gp, int64_t* tk, double* tv
         }
         PassArgs<T> c = a;
         c.red.out = P->res_d + 2 * k;
-        CGH_TRY(run_col<T>(P, COL_GS, c, 1));
+        if constexpr (sizeof(T) == 4) {
+            if (fast) CGH_TRY(fast_col(P, c));
+            else CGH_TRY(run_col<T>(P, COL_GS, c, 1));
+        } else {
+            CGH_TRY(run_col<T>(P, COL_GS, c, 1));
+        }
         if (has_progress || has_cancel) CGH_TRY(pq.push(k));
         const bool last = (k == iters - 1);
         PassArgs<T> r = a;
         r.quantize = (gp->quantize_each_iteration || last) ? 1 : 0;
         r.idx_out = last ? P->idx.p : nullptr;
         r.field_out = last ? field_dev : nullptr;
-        CGH_TRY(run_row<T>(P, ROW_HOLO, r, 1));
+        bool done_fast = false;
+        if constexpr (sizeof(T) == 4) {
+            if (fast && !r.quantize && !r.field_out) {
+                CGH_TRY(fast_row(P, r));
+                done_fast = true;
+            }
+        }
+        if (!done_fast) CGH_TRY(run_row<T>(P, ROW_HOLO, r, 1));
         executed = k + 1;
         if (has_progress || has_cancel) CGH_TRY(pq.poll(false));
     }

@@ -1,5 +1,6 @@
 // Host runtime shared by the C-ABI translation units: plans, buffers, errors.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -66,6 +67,7 @@ struct cgh_plan {
     cgh::DevBuf states64, states32, tw_row, tw_col, q_row, q_col;
     cgh::DevBuf data, tgt, beam, idx, field, partials, counter, stats, stage, mask, frame_rng, intensity;
     cgh::DevBuf sa_buf;   // search state (SA/DBS)
+    void* fast = nullptr; // FastState of the pipelined complex64 GS passes (fast.cu)
     int idx_bytes = 1;
     bool has_beam = false, target_ready = false;
     // mapped host results
@@ -93,6 +95,14 @@ int plan_upload_target(cgh_plan* P, const double* target, const uint8_t* mask, c
 
 template <class T>
 PassArgs<T> base_args(cgh_plan* P);
+
+// Pipelined complex64 GS passes (fast.cu): eligibility, per-plan setup, launches.
+bool fast_eligible(cgh_plan* P);
+int fast_prepare(cgh_plan* P);
+int fast_row(cgh_plan* P, const PassArgs<float>& a);
+int fast_col(cgh_plan* P, const PassArgs<float>& a);
+void fast_free(cgh_plan* P);
+void fast_invalidate_target(cgh_plan* P);
 
 // Record a timing event before (start) / after a pass launch. Pass ids:
 // row modes 0..7, column modes 8 + mode, search kernels 16+.
