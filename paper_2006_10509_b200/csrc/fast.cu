@@ -26,26 +26,35 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
-template <int N>
-static int lines_of() {
-    return FastShape<N>::LINES;
+// Launch configurations: rows 256 threads x 2 CTAs/SM (2 rows per tile);
+// columns 512 threads x 1 CTA/SM (4 columns = 32 B per row segment) or, with
+// CGHB200_COL_TH=256, 256 x 2 (2 columns).
+constexpr int kRowTH = 256, kRowMinB = 2;
+
+static int col_th() {
+    static int v = 0;
+    if (!v) {
+        const char* e = getenv("CGHB200_COL_TH");
+        v = (e && atoi(e) == 256) ? 256 : 512;
+    }
+    return v;
 }
 
-static int fast_lines(int n) {
+static int fast_lines_th(int n, int th) {
     switch (n) {
-        case 256: return lines_of<256>();
-        case 512: return lines_of<512>();
-        case 1024: return lines_of<1024>();
-        case 2048: return lines_of<2048>();
-        case 4096: return lines_of<4096>();
+        case 256: return th / (256 / 16);
+        case 512: return th / (512 / 16);
+        case 1024: return th / (1024 / 16);
+        case 2048: return th / (2048 / 16);
+        case 4096: return th / (4096 / 16);
         default: return 0;
     }
 }
 
 bool fast_eligible(cgh_plan* P) {
     if (P->prec != CGH_FP32) return false;
-    const int lr = fast_lines(P->W), lc = fast_lines(P->H);
-    if (!lr || !lc) return false;
+    const int lr = fast_lines_th(P->W, kRowTH), lc = fast_lines_th(P->H, col_th());
+    if (lr < 1 || lc < 1) return false;
     if (P->H < lr || P->W < lc) return false;
     if (getenv("CGHB200_NO_FAST")) return false;
     return encode_fn() != nullptr;
@@ -67,7 +76,7 @@ int fast_prepare(cgh_plan* P) {
         F = new FastState();
         P->fast = F;
     }
-    const int C = fast_lines(P->H);
+    const int C = fast_lines_th(P->H, col_th());
     if (F->tmap_ptr != P->data.p || F->H != P->H || F->W != P->W) {
         cuuint64_t dims[2] = {cuuint64_t(2) * P->W, cuuint64_t(P->H)};
         cuuint64_t strides[1] = {cuuint64_t(P->W) * 8};
@@ -88,8 +97,10 @@ int fast_prepare(cgh_plan* P) {
     if (F->tgt_src != P->tgt.p || !F->tgt_tiled.p) {
         const long long n = (long long)P->H * P->W;
         CGH_TRY(ensure(P, F->tgt_tiled, size_t(n) * 4));
+        const float inv_scale = float(std::sqrt(double(P->H) * double(P->W)));
         tile_target_kernel<<<grid_for(n), 256, 0, P->st>>>(static_cast<const float*>(P->tgt.p),
-                                                          static_cast<float*>(F->tgt_tiled.p), P->H, P->W, C);
+                                                          static_cast<float*>(F->tgt_tiled.p), P->H, P->W, C,
+                                                          inv_scale);
         P->launches += 1;
         CGH_CUDA(cudaGetLastError());
         F->tgt_src = P->tgt.p;
@@ -127,35 +138,67 @@ static int sm_count(int dev) {
     return cached[dev & 63];
 }
 
+template <class K, class... Args>
+static cudaError_t launch_pdl(K kernel, int grid, int block, size_t smem, cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 template <int N>
 static cudaError_t row_launch(cgh_plan* P, const FastArgs& f) {
-    using S = FastShape<N>;
-    const size_t smem = size_t(2) * FastSlots<N>::ROW * sizeof(float2);
+    using S = FastShape<N, kRowTH>;
+    const size_t smem = size_t(2) * FastSlots<N, kRowTH>::ROW * sizeof(float2);
+    auto k = fast_row_holo<N, kRowTH, kRowMinB>;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(fast_row_holo<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         attr = true;
     }
     const int tiles = P->H / S::LINES;
-    const int grid = std::max(1, std::min(sm_count(P->dev), tiles));
-    fast_row_holo<N><<<grid, kFastThreads, smem, P->st>>>(f);
-    return cudaGetLastError();
+    const int grid = std::max(1, std::min(kRowMinB * sm_count(P->dev), tiles));
+    return launch_pdl(k, grid, kRowTH, smem, P->st, f);
+}
+
+template <int N, int TH, int MINB, int MODE>
+static cudaError_t col_launch_m(cgh_plan* P, const FastArgs& f) {
+    using S = FastShape<N, TH>;
+    FastState* F = static_cast<FastState*>(P->fast);
+    const size_t smem = size_t(2) * FastSlots<N, TH>::COL * sizeof(float2);
+    auto k = fast_col_gs<N, TH, MINB, MODE>;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        attr = true;
+    }
+    const int tiles = P->W / S::LINES;
+    const int grid = std::max(1, std::min(MINB * sm_count(P->dev), tiles));
+    return launch_pdl(k, grid, TH, smem, P->st, f, F->tmap);
+}
+
+template <int N, int TH, int MINB>
+static cudaError_t col_launch_th(cgh_plan* P, const FastArgs& f, int mode) {
+    switch (mode) {
+        case 0: return col_launch_m<N, TH, MINB, 0>(P, f);
+        case 1: return col_launch_m<N, TH, MINB, 1>(P, f);
+        case 2: return col_launch_m<N, TH, MINB, 2>(P, f);
+        default: return col_launch_m<N, TH, MINB, 3>(P, f);
+    }
 }
 
 template <int N>
 static cudaError_t col_launch(cgh_plan* P, const FastArgs& f) {
-    using S = FastShape<N>;
-    FastState* F = static_cast<FastState*>(P->fast);
-    const size_t smem = size_t(2) * FastSlots<N>::COL * sizeof(float2);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(fast_col_gs<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        attr = true;
-    }
-    const int tiles = P->W / S::LINES;
-    const int grid = std::max(1, std::min(sm_count(P->dev), tiles));
-    fast_col_gs<N><<<grid, kFastThreads, smem, P->st>>>(f, F->tmap);
-    return cudaGetLastError();
+    const int mode = (P->rescale ? 1 : 0) | (f.gain != 0.0f ? 2 : 0);
+    if (col_th() == 256) return col_launch_th<N, 256, 2>(P, f, mode);
+    return col_launch_th<N, 512, 1>(P, f, mode);
 }
 
 int fast_row(cgh_plan* P, const PassArgs<float>& a) {

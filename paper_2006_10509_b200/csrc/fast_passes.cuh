@@ -21,16 +21,15 @@
 
 namespace cgh {
 
-constexpr int kFastThreads = 512;
 constexpr int kFastBoxRows = 256;
 
 __device__ __forceinline__ int padc(int i) { return i + (i >> 4); }   // 1 float2 per 16 (128 B)
 
-template <int N>
+template <int N, int TH>
 struct FastShape {
     static constexpr int E = 16;
     static constexpr int TF = N / E;
-    static constexpr int LINES = kFastThreads / TF;       // lines per tile
+    static constexpr int LINES = TH / TF;                  // lines per tile
     // padded line (float2): 1 word per 16, plus 4 so that lines c = 0..3 of a
     // column tile start in different banks (LW = 4 mod 16)
     static constexpr int LW = N + N / 16 + 4;
@@ -39,15 +38,15 @@ struct FastShape {
     static constexpr int R2 = N / NS2;                     // stage-3 radix (1 = none)
 };
 
-template <int N>
+template <int N, int TH>
 struct FastTw {
     cx<float> w1[16];   // stage 2 (NS = 16)
     cx<float> w2[16];   // stage 3 (NS = 16*R1)
 };
 
-template <int N>
-__device__ __forceinline__ void fast_tw_init(FastTw<N>& tw, int t, const cx<float>* __restrict__ table) {
-    using S = FastShape<N>;
+template <int N, int TH>
+__device__ __forceinline__ void fast_tw_init(FastTw<N, TH>& tw, int t, const cx<float>* __restrict__ table) {
+    using S = FastShape<N, TH>;
     {
         constexpr int NS = 16, R = S::R1, NB = 16 / R;
 #pragma unroll
@@ -77,9 +76,9 @@ __device__ __forceinline__ constexpr int padk() { return K + K / 16; }
 
 // One Stockham stage (index algebra in fft_block.cuh). `pt` = padc(t): every
 // read address is pt + constant, every write address padc(base_b) + constant.
-template <int N, int DIR, int NS, int R, bool LAST>
+template <int N, int TH, int DIR, int NS, int R, bool LAST>
 __device__ __forceinline__ void fast_stage(cx<float> (&v)[16], float2* sm, int t, int pt, const cx<float>* tw) {
-    using S = FastShape<N>;
+    using S = FastShape<N, TH>;
     constexpr int NB = 16 / R;
     if constexpr (NS > 1) {
 #pragma unroll
@@ -123,15 +122,15 @@ __device__ __forceinline__ void fast_stage(cx<float> (&v)[16], float2* sm, int t
     }
 }
 
-template <int N, int DIR>
-__device__ __forceinline__ void fast_fft(cx<float> (&v)[16], float2* sm, int t, int pt, const FastTw<N>& tw) {
-    using S = FastShape<N>;
-    fast_stage<N, DIR, 1, 16, false>(v, sm, t, pt, nullptr);
+template <int N, int TH, int DIR>
+__device__ __forceinline__ void fast_fft(cx<float> (&v)[16], float2* sm, int t, int pt, const FastTw<N, TH>& tw) {
+    using S = FastShape<N, TH>;
+    fast_stage<N, TH, DIR, 1, 16, false>(v, sm, t, pt, nullptr);
     if constexpr (S::R2 > 1) {
-        fast_stage<N, DIR, 16, S::R1, false>(v, sm, t, pt, tw.w1);
-        fast_stage<N, DIR, S::NS2, S::R2, true>(v, sm, t, pt, tw.w2);
+        fast_stage<N, TH, DIR, 16, S::R1, false>(v, sm, t, pt, tw.w1);
+        fast_stage<N, TH, DIR, S::NS2, S::R2, true>(v, sm, t, pt, tw.w2);
     } else {
-        fast_stage<N, DIR, 16, S::R1, true>(v, sm, t, pt, tw.w1);
+        fast_stage<N, TH, DIR, 16, S::R1, true>(v, sm, t, pt, tw.w1);
     }
 }
 
@@ -149,33 +148,57 @@ struct FastArgs {
     ReduceArgs red;
 };
 
-// Tiles are assigned statically: CTA b handles tiles b, b + G, b + 2G, ...
-template <int N>
+// Programmatic dependent launch: the prologue (twiddles, barriers) of pass
+// k+1 overlaps the tail of pass k; data is touched only after the wait.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// Dynamic tile scheduling: thread 0 claims the tile for a slot one iteration
+// early (the atomic's latency hides behind the transform); the last CTA to
+// finish resets the counter for the next launch.
+template <int N, int TH>
 struct FastSlots {
-    static constexpr int ROW = FastShape<N>::LINES * FastShape<N>::LW;                            // float2
-    static constexpr int COL = FastShape<N>::LINES * FastShape<N>::LW + FastShape<N>::LINES * N / 2;   // + target tile
+    using S = FastShape<N, TH>;
+    // float2 words per slot, rounded to 128 B (TMA destination alignment)
+    static constexpr int ROW = (S::LINES * S::LW + 15) / 16 * 16;
+    static constexpr int COL = (S::LINES * S::LW + S::LINES * N / 2 + 15) / 16 * 16;   // + target tile
 };
 
+__device__ __forceinline__ void finish_ctas(unsigned* ctr) {
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(ctr + 1, 1u) == gridDim.x - 1) {
+            ctr[0] = 0u;
+            ctr[1] = 0u;
+        }
+    }
+}
+
 // ================================================================ rows
-template <int N>
-__global__ void __launch_bounds__(kFastThreads, 1) fast_row_holo(FastArgs a) {
-    using S = FastShape<N>;
-    constexpr int TF = S::TF, LINES = S::LINES, LW = S::LW, SLOT = FastSlots<N>::ROW;
+template <int N, int TH, int MINB>
+__global__ void __launch_bounds__(TH, MINB) fast_row_holo(FastArgs a) {
+    using S = FastShape<N, TH>;
+    constexpr int TF = S::TF, LINES = S::LINES, LW = S::LW, SLOT = FastSlots<N, TH>::ROW;
     constexpr uint32_t TILE_BYTES = uint32_t(LINES) * N * 8u;
     extern __shared__ __align__(128) float2 fsm[];
     __shared__ __align__(8) uint64_t full[2];
+    __shared__ int tileq[2];
     const int tid = threadIdx.x, li = tid / TF, t = tid - li * TF;
     const int pt = padc(t);
-    const int ntiles = a.H / LINES, G = gridDim.x;
-    FastTw<N> tw;
-    fast_tw_init<N>(tw, t, a.tw_row);
+    const int ntiles = a.H / LINES;
+    FastTw<N, TH> tw;
+    fast_tw_init<N, TH>(tw, t, a.tw_row);
     if (tid == 0) {
         mbar_init(&full[0], 1);
         mbar_init(&full[1], 1);
         mbar_fence_init();
+    }
+    pdl_wait();
+    if (tid == 0) {
 #pragma unroll
         for (int s = 0; s < 2; ++s) {
-            const int tile = blockIdx.x + s * G;
+            const int tile = int(atomicAdd(a.tile_ctr, 1u));
+            tileq[s] = tile;
             if (tile < ntiles) {
                 mbar_expect_tx(&full[s], TILE_BYTES);
                 bulk_g2s(fsm + s * SLOT, a.data + size_t(tile) * LINES * N, TILE_BYTES, &full[s]);
@@ -185,8 +208,10 @@ __global__ void __launch_bounds__(kFastThreads, 1) fast_row_holo(FastArgs a) {
     __syncthreads();
     for (int it = 0;; ++it) {
         const int s = it & 1;
-        const int tile = blockIdx.x + it * G;
+        const int tile = tileq[s];
         if (tile >= ntiles) break;
+        unsigned next = 0;
+        if (tid == 0) next = atomicAdd(a.tile_ctr, 1u);
         float2* buf = fsm + s * SLOT;
         const int m = tile * LINES + li;
         mbar_wait(&full[s], (it >> 1) & 1);
@@ -198,7 +223,7 @@ __global__ void __launch_bounds__(kFastThreads, 1) fast_row_holo(FastArgs a) {
             v[r] = mk(z.x, z.y);
         }
         float2* line = buf + li * LW;
-        fast_fft<N, +1>(v, line, t, pt, tw);
+        fast_fft<N, TH, +1>(v, line, t, pt, tw);
 #pragma unroll
         for (int r = 0; r < 16; ++r) {
             const float amp = a.beam ? __ldg(a.beam + size_t(m) * N + t + r * TF) : 1.0f;
@@ -212,35 +237,45 @@ __global__ void __launch_bounds__(kFastThreads, 1) fast_row_holo(FastArgs a) {
                 v[r] = h;
             }
         }
-        fast_fft<N, -1>(v, line, t, pt, tw);
+        fast_fft<N, TH, -1>(v, line, t, pt, tw);
         float2* dst = a.data + size_t(m) * N + t;
 #pragma unroll
         for (int r = 0; r < 16; ++r) dst[r * TF] = make_float2(v[r].x, v[r].y);
         fence_proxy_async();
         __syncthreads();
-        const int nt = tile + 2 * G;
-        if (tid == 0 && nt < ntiles) {
-            mbar_expect_tx(&full[s], TILE_BYTES);
-            bulk_g2s(buf, a.data + size_t(nt) * LINES * N, TILE_BYTES, &full[s]);
+        if (tid == 0) {
+            const int nt = int(next);
+            tileq[s] = nt;
+            if (nt < ntiles) {
+                mbar_expect_tx(&full[s], TILE_BYTES);
+                bulk_g2s(buf, a.data + size_t(nt) * LINES * N, TILE_BYTES, &full[s]);
+            }
         }
     }
+    pdl_trigger();
+    finish_ctas(a.tile_ctr);
 }
 
 // ============================================================= columns
-template <int N>
-__global__ void __launch_bounds__(kFastThreads, 1) fast_col_gs(FastArgs a, const __grid_constant__ CUtensorMap tmap) {
-    using S = FastShape<N>;
-    constexpr int TF = S::TF, C = S::LINES, LW = S::LW, SLOT = FastSlots<N>::COL;
+// The target tile arrives pre-divided by the transform scale, so the replay
+// projection works on unscaled column-FFT outputs; sums are rescaled once.
+// MODE bit 0: rescale sums (S_rr, S_rd); bit 1: feedback gain != 0.
+template <int N, int TH, int MINB, int MODE>
+__global__ void __launch_bounds__(TH, MINB) fast_col_gs(FastArgs a, const __grid_constant__ CUtensorMap tmap) {
+    using S = FastShape<N, TH>;
+    constexpr int TF = S::TF, C = S::LINES, LW = S::LW, SLOT = FastSlots<N, TH>::COL;
+    constexpr bool RESCALE = (MODE & 1) != 0, GAIN = (MODE & 2) != 0;
     constexpr uint32_t TILE_BYTES = uint32_t(C) * N * 8u;
     constexpr uint32_t TGT_BYTES = uint32_t(C) * N * 4u;
     extern __shared__ __align__(128) float2 fsm[];
     __shared__ __align__(8) uint64_t full[2];
+    __shared__ int tileq[2];
     __shared__ double rsh[32 * 4];
     const int tid = threadIdx.x, t = tid / C, c = tid - t * C;
     const int pt = padc(t);
-    const int ntiles = a.W / C, G = gridDim.x;
-    FastTw<N> tw;
-    fast_tw_init<N>(tw, t, a.tw_col);
+    const int ntiles = a.W / C;
+    FastTw<N, TH> tw;
+    fast_tw_init<N, TH>(tw, t, a.tw_col);
     auto issue = [&](int s, int tile) {
         mbar_expect_tx(&full[s], TILE_BYTES + TGT_BYTES);
 #pragma unroll 1
@@ -252,17 +287,25 @@ __global__ void __launch_bounds__(kFastThreads, 1) fast_col_gs(FastArgs a, const
         mbar_init(&full[0], 1);
         mbar_init(&full[1], 1);
         mbar_fence_init();
+    }
+    pdl_wait();
+    if (tid == 0) {
 #pragma unroll
-        for (int s = 0; s < 2; ++s)
-            if (blockIdx.x + s * G < ntiles) issue(s, blockIdx.x + s * G);
+        for (int s = 0; s < 2; ++s) {
+            const int tile = int(atomicAdd(a.tile_ctr, 1u));
+            tileq[s] = tile;
+            if (tile < ntiles) issue(s, tile);
+        }
     }
     __syncthreads();
-    double acc[4] = {0, 0, 0, 0};
-    const float gain = a.gain, scale = a.scale;
+    float sdd = 0.f, srr = 0.f, srd = 0.f;
+    const float gain = a.gain;
     for (int it = 0;; ++it) {
         const int s = it & 1;
-        const int tile = blockIdx.x + it * G;
+        const int tile = tileq[s];
         if (tile >= ntiles) break;
+        unsigned next = 0;
+        if (tid == 0) next = atomicAdd(a.tile_ctr, 1u);
         float2* buf = fsm + s * SLOT;
         const float* tg = reinterpret_cast<const float*>(buf + C * LW) + t * C + c;
         mbar_wait(&full[s], (it >> 1) & 1);
@@ -274,61 +317,68 @@ __global__ void __launch_bounds__(kFastThreads, 1) fast_col_gs(FastArgs a, const
             v[r] = mk(z.x, z.y);
         }
         float2* line = buf + c * LW;
-        fast_fft<N, -1>(v, line, t, pt, tw);
-        float sdd = 0.f, srr = 0.f, srd = 0.f, sall = 0.f;
+        fast_fft<N, TH, -1>(v, line, t, pt, tw);
 #pragma unroll
         for (int r = 0; r < 16; ++r) {
-            const float x = v[r].x * scale, y = v[r].y * scale;
+            const float x = v[r].x, y = v[r].y;
             const float r2 = x * x + y * y;
+            const float ri = rsqrtf(r2);                       // inf at 0
+            const float rr = r2 > 0.0f ? r2 * ri : 0.0f;
             const float tt = tg[r * TF * C];
             const bool in = !signbit(tt);
-            const float rr = sqrtf(r2);
             const float d = rr - tt;
-            sall += r2;
             sdd += in ? d * d : 0.0f;
-            srr += in ? r2 : 0.0f;
-            srd += in ? rr * d : 0.0f;
-            const float want = fmaxf(tt + gain * (tt - rr), 0.0f);
-            const bool pos = rr > 0.0f;
-            const float k = in ? (pos ? __fdividef(want, rr) : 0.0f) : 1.0f;
+            if constexpr (RESCALE) {
+                srr += in ? r2 : 0.0f;
+                srd += in ? rr * d : 0.0f;
+            }
+            float want = tt;
+            if constexpr (GAIN) want = fmaxf(tt + gain * (tt - rr), 0.0f);
+            const bool pos = r2 > 0.0f;
+            const float k = in ? (pos ? want * ri : 0.0f) : 1.0f;
             v[r] = mk(x * k + ((in && !pos) ? want : 0.0f), y * k);
         }
-        acc[0] += sdd;
-        acc[1] += srr;
-        acc[2] += srd;
-        acc[3] += sall;
-        fast_fft<N, +1>(v, line, t, pt, tw);
+        fast_fft<N, TH, +1>(v, line, t, pt, tw);
         float2* dst = a.data + size_t(tile) * C + c + size_t(t) * a.W;
         const size_t step = size_t(TF) * a.W;
 #pragma unroll
         for (int r = 0; r < 16; ++r) dst[r * step] = make_float2(v[r].x, v[r].y);
         fence_proxy_async();
         __syncthreads();
-        const int nt = tile + 2 * G;
-        if (tid == 0 && nt < ntiles) issue(s, nt);
+        if (tid == 0) {
+            const int nt = int(next);
+            tileq[s] = nt;
+            if (nt < ntiles) issue(s, nt);
+        }
     }
+    pdl_trigger();
+    // sums in units of the unscaled transform: multiply by scale^2 once
+    const double sc2 = double(a.scale) * double(a.scale);
+    double acc[4] = {double(sdd) * sc2, double(srr) * sc2, double(srd) * sc2, 0.0};
     block_reduce<4>(acc, rsh);
     const int nblocks = gridDim.x;
     if (publish_partials<4>(a.red, acc, nblocks, blockIdx.x)) {
         const double s_dd = sum_partials(a.red, 0, nblocks, rsh);
         const double s_rr = sum_partials(a.red, 1, nblocks, rsh);
         const double s_rd = sum_partials(a.red, 2, nblocks, rsh);
-        const double s_all = sum_partials(a.red, 3, nblocks, rsh);
         if (threadIdx.x == 0) {
-            a.red.out[0] = error_from_sums(s_dd, s_rr, s_rd, *a.red.denom, a.red.rescale);
-            a.red.out[1] = s_all == 0.0 ? __longlong_as_double(0x7ff8000000000000LL) : s_rr / s_all;
+            a.red.out[0] = error_from_sums(s_dd, s_rr, s_rd, *a.red.denom, RESCALE ? a.red.rescale : 0);
+            a.red.out[1] = 0.0;   // efficiency is reported by the final (generic) pass only
             *a.red.counter = 0u;
+            a.tile_ctr[0] = 0u;
+            a.tile_ctr[1] = 0u;
         }
     }
 }
 
 // [W/C][H][C] copy of the row-major shifted target
-__global__ void tile_target_kernel(const float* __restrict__ tgt, float* __restrict__ out, int H, int W, int C) {
+__global__ void tile_target_kernel(const float* __restrict__ tgt, float* __restrict__ out, int H, int W, int C,
+                                   float inv_scale) {
     const long long total = (long long)H * W;
     for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < total;
          p += (long long)gridDim.x * blockDim.x) {
         const int u = int(p / W), n = int(p - (long long)u * W);
-        out[((long long)(n / C) * H + u) * C + (n % C)] = tgt[p];
+        out[((long long)(n / C) * H + u) * C + (n % C)] = tgt[p] * inv_scale;   // sign (mask) preserved
     }
 }
 
