@@ -54,7 +54,7 @@ static int fast_lines_th(int n, int th) {
 bool fast_eligible(cgh_plan* P) {
     if (P->prec != CGH_FP32) return false;
     const int lr = fast_lines_th(P->W, kRowTH), lc = fast_lines_th(P->H, col_th());
-    if (lr < 1 || lc < 1) return false;
+    if (lr < 1 || lc < 1 || P->W < 512) return false;   // row groups are whole warps (W >= 512)
     if (P->H < lr || P->W < lc) return false;
     if (getenv("CGHB200_NO_FAST")) return false;
     return encode_fn() != nullptr;
@@ -129,6 +129,8 @@ static FastArgs fast_args(cgh_plan* P, const PassArgs<float>& a) {
     f.scale = a.scale;
     f.tile_ctr = static_cast<unsigned*>(F->ctr.p);
     f.red = a.red;
+    const char* dbg = getenv("CGHB200_FAST_DEBUG");
+    f.debug = dbg ? atoi(dbg) : 0;
     return f;
 }
 
@@ -153,17 +155,42 @@ static cudaError_t launch_pdl(K kernel, int grid, int block, size_t smem, cudaSt
     return cudaLaunchKernelEx(&cfg, kernel, args...);
 }
 
+template <int N, int MINB>
+static cudaError_t row_launch_s(cgh_plan* P, const FastArgs& f) {
+    using S = FastShape<N, kRowTH>;
+    const size_t smem = (size_t(TwTables<N, kRowTH>::WORDS) + size_t(S::LINES) * ((S::LW + 15) / 16 * 16)) * sizeof(float2);
+    auto k = fast_row_holo_s<N, kRowTH, MINB>;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        attr = true;
+    }
+    const int grid = std::max(1, std::min(MINB * sm_count(P->dev), P->H / S::LINES));
+    return launch_pdl(k, grid, kRowTH, smem, P->st, f);
+}
+
+static int row_variant() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("CGHB200_ROW_VARIANT");
+        v = e ? atoi(e) : 0;
+    }
+    return v;
+}
+
 template <int N>
 static cudaError_t row_launch(cgh_plan* P, const FastArgs& f) {
+    if (row_variant() == 3) return row_launch_s<N, 3>(P, f);
+    if (row_variant() == 4) return row_launch_s<N, 4>(P, f);
     using S = FastShape<N, kRowTH>;
-    const size_t smem = size_t(2) * FastSlots<N, kRowTH>::ROW * sizeof(float2);
+    const size_t smem = size_t(2) * S::LINES * ((S::LW + 15) / 16 * 16) * sizeof(float2);
     auto k = fast_row_holo<N, kRowTH, kRowMinB>;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         attr = true;
     }
-    const int tiles = P->H / S::LINES;
+    const int tiles = P->H / S::LINES;   // row groups per CTA = S::LINES
     const int grid = std::max(1, std::min(kRowMinB * sm_count(P->dev), tiles));
     return launch_pdl(k, grid, kRowTH, smem, P->st, f);
 }
@@ -206,7 +233,6 @@ int fast_row(cgh_plan* P, const PassArgs<float>& a) {
     if (P->profiling) CGH_TRY(prof_mark(P, ROW_HOLO, true));
     cudaError_t e;
     switch (P->W) {
-        case 256: e = row_launch<256>(P, f); break;
         case 512: e = row_launch<512>(P, f); break;
         case 1024: e = row_launch<1024>(P, f); break;
         case 2048: e = row_launch<2048>(P, f); break;

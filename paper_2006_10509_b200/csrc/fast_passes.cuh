@@ -76,16 +76,40 @@ __device__ __forceinline__ constexpr int padk() { return K + K / 16; }
 
 // One Stockham stage (index algebra in fft_block.cuh). `pt` = padc(t): every
 // read address is pt + constant, every write address padc(base_b) + constant.
-template <int N, int TH, int DIR, int NS, int R, bool LAST>
-__device__ __forceinline__ void fast_stage(cx<float> (&v)[16], float2* sm, int t, int pt, const cx<float>* tw) {
+// named barrier over the threads sharing one exchange buffer
+__device__ __forceinline__ void group_sync(int id, int count) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+// Twiddle sources: per-thread registers (RegTw) or a shared-memory table
+// laid out [r][j mod NS] (SmemTw; lanes read consecutive entries).
+struct RegTw {
+    const cx<float>* w;
+    template <int NS, int R, int TF>
+    __device__ __forceinline__ cx<float> get(int, int b, int r) const { return w[b * R + r]; }
+};
+struct SmemTw {
+    const float2* tab;   // this stage's table
+    template <int NS, int R, int TF>
+    __device__ __forceinline__ cx<float> get(int t, int b, int r) const {
+        const float2 z = tab[r * NS + ((t + b * TF) & (NS - 1))];
+        return mk(z.x, z.y);
+    }
+};
+
+template <int N, int TH, int DIR, int NS, int R, bool LAST, class TW>
+__device__ __forceinline__ void fast_stage(cx<float> (&v)[16], float2* sm, int t, int pt, const TW& tw, int bid,
+                                           int bcount) {
     using S = FastShape<N, TH>;
     constexpr int NB = 16 / R;
     if constexpr (NS > 1) {
 #pragma unroll
         for (int b = 0; b < NB; ++b)
 #pragma unroll
-            for (int r = 1; r < R; ++r)
-                v[b * R + r] = DIR < 0 ? cmul(v[b * R + r], tw[b * R + r]) : cmulc(v[b * R + r], tw[b * R + r]);
+            for (int r = 1; r < R; ++r) {
+                const cx<float> w = tw.template get<NS, R, S::TF>(t, b, r);
+                v[b * R + r] = DIR < 0 ? cmul(v[b * R + r], w) : cmulc(v[b * R + r], w);
+            }
     }
 #pragma unroll
     for (int b = 0; b < NB; ++b) Dft<R, DIR, 1, float>::run(&v[b * R]);
@@ -99,8 +123,8 @@ __device__ __forceinline__ void fast_stage(cx<float> (&v)[16], float2* sm, int t
 #pragma unroll
                 for (int r = 0; r < R; ++r) v[b + r * NB] = tmp[b * R + r];
         }
-    } else {
-        __syncthreads();
+    } else if (bid >= 0) {   // bid < 0: exchange skipped (timing experiments only)
+        group_sync(bid, bcount);
 #pragma unroll
         for (int b = 0; b < NB; ++b) {
             const int j = t + b * S::TF;
@@ -108,7 +132,7 @@ __device__ __forceinline__ void fast_stage(cx<float> (&v)[16], float2* sm, int t
 #pragma unroll
             for (int r = 0; r < R; ++r) wp[r * NS + (r * NS) / 16] = make_float2(v[b * R + r].x, v[b * R + r].y);
         }
-        __syncthreads();
+        group_sync(bid, bcount);
         constexpr int RN = (N / (NS * R) >= 16) ? 16 : N / (NS * R);   // next radix
         constexpr int NBN = 16 / RN;
         const float2* rp = sm + pt;
@@ -123,14 +147,49 @@ __device__ __forceinline__ void fast_stage(cx<float> (&v)[16], float2* sm, int t
 }
 
 template <int N, int TH, int DIR>
-__device__ __forceinline__ void fast_fft(cx<float> (&v)[16], float2* sm, int t, int pt, const FastTw<N, TH>& tw) {
+__device__ __forceinline__ void fast_fft(cx<float> (&v)[16], float2* sm, int t, int pt, const FastTw<N, TH>& tw,
+                                         int bid = 0, int bcount = TH) {
     using S = FastShape<N, TH>;
-    fast_stage<N, TH, DIR, 1, 16, false>(v, sm, t, pt, nullptr);
+    fast_stage<N, TH, DIR, 1, 16, false>(v, sm, t, pt, RegTw{nullptr}, bid, bcount);
     if constexpr (S::R2 > 1) {
-        fast_stage<N, TH, DIR, 16, S::R1, false>(v, sm, t, pt, tw.w1);
-        fast_stage<N, TH, DIR, S::NS2, S::R2, true>(v, sm, t, pt, tw.w2);
+        fast_stage<N, TH, DIR, 16, S::R1, false>(v, sm, t, pt, RegTw{tw.w1}, bid, bcount);
+        fast_stage<N, TH, DIR, S::NS2, S::R2, true>(v, sm, t, pt, RegTw{tw.w2}, bid, bcount);
     } else {
-        fast_stage<N, TH, DIR, 16, S::R1, true>(v, sm, t, pt, tw.w1);
+        fast_stage<N, TH, DIR, 16, S::R1, true>(v, sm, t, pt, RegTw{tw.w1}, bid, bcount);
+    }
+}
+
+// Shared-memory twiddle tables: stage 2 [R1][16], stage 3 [R2][NS2] (float2).
+template <int N, int TH>
+struct TwTables {
+    using S = FastShape<N, TH>;
+    static constexpr int T2 = S::R1 * 16;
+    static constexpr int T3 = S::R2 > 1 ? S::R2 * S::NS2 : 0;
+    static constexpr int WORDS = (T2 + T3 + 15) / 16 * 16;
+    __device__ static void load(float2* tab, const cx<float>* __restrict__ table) {
+        for (int i = threadIdx.x; i < T2; i += blockDim.x) {
+            const int r = i / 16, jm = i % 16;
+            const cx<float> z = ldg_cx(table + jm * r * (N / (16 * S::R1)));
+            tab[i] = make_float2(z.x, z.y);
+        }
+        for (int i = threadIdx.x; i < T3; i += blockDim.x) {
+            const int r = i / S::NS2, jm = i % S::NS2;
+            const cx<float> z = ldg_cx(table + jm * r * (N / (S::NS2 * S::R2)));
+            tab[T2 + i] = make_float2(z.x, z.y);
+        }
+    }
+};
+
+template <int N, int TH, int DIR>
+__device__ __forceinline__ void fast_fft_s(cx<float> (&v)[16], float2* sm, int t, int pt, const float2* tab, int bid,
+                                           int bcount) {
+    using S = FastShape<N, TH>;
+    fast_stage<N, TH, DIR, 1, 16, false>(v, sm, t, pt, RegTw{nullptr}, bid, bcount);
+    if constexpr (S::R2 > 1) {
+        fast_stage<N, TH, DIR, 16, S::R1, false>(v, sm, t, pt, SmemTw{tab}, bid, bcount);
+        fast_stage<N, TH, DIR, S::NS2, S::R2, true>(v, sm, t, pt, SmemTw{tab + TwTables<N, TH>::T2}, bid, bcount);
+    } else {
+        fast_stage<N, TH, DIR, 16, S::R1, true>(v, sm, t, pt, SmemTw{tab}, bid, bcount);
     }
 }
 
@@ -146,6 +205,7 @@ struct FastArgs {
     float gain, scale;
     unsigned* tile_ctr;           // [0] tile counter, [1] finished CTAs
     ReduceArgs red;
+    int debug;                    // experiments: 1 = no transforms, 2 = no loads/stores
 };
 
 // Programmatic dependent launch: the prologue (twiddles, barriers) of pass
@@ -175,55 +235,64 @@ __device__ __forceinline__ void finish_ctas(unsigned* ctr) {
 }
 
 // ================================================================ rows
+// Each group of TF threads (one image row) runs its own two-slot bulk-copy
+// pipeline with its own barriers and claims rows independently, so the
+// groups of a CTA drift apart and overlap exchange and arithmetic phases.
 template <int N, int TH, int MINB>
 __global__ void __launch_bounds__(TH, MINB) fast_row_holo(FastArgs a) {
     using S = FastShape<N, TH>;
-    constexpr int TF = S::TF, LINES = S::LINES, LW = S::LW, SLOT = FastSlots<N, TH>::ROW;
-    constexpr uint32_t TILE_BYTES = uint32_t(LINES) * N * 8u;
+    constexpr int TF = S::TF, GROUPS = S::LINES, LW = S::LW;
+    constexpr int SLOT = (LW + 15) / 16 * 16;   // one padded line, 128-B aligned
+    constexpr uint32_t LINE_BYTES = uint32_t(N) * 8u;
+    static_assert(TF % 32 == 0, "row groups must be whole warps");
     extern __shared__ __align__(128) float2 fsm[];
-    __shared__ __align__(8) uint64_t full[2];
-    __shared__ int tileq[2];
-    const int tid = threadIdx.x, li = tid / TF, t = tid - li * TF;
+    __shared__ __align__(8) uint64_t full[GROUPS][2];
+    __shared__ int lineq[GROUPS][2];
+    const int tid = threadIdx.x, g = tid / TF, t = tid - g * TF;
+    const bool lead = (t == 0);
     const int pt = padc(t);
-    const int ntiles = a.H / LINES;
+    const int nlines = a.H;
+    const int bid = 1 + g;
+    float2* slots = fsm + g * 2 * SLOT;
     FastTw<N, TH> tw;
     fast_tw_init<N, TH>(tw, t, a.tw_row);
-    if (tid == 0) {
-        mbar_init(&full[0], 1);
-        mbar_init(&full[1], 1);
+    if (lead) {
+        mbar_init(&full[g][0], 1);
+        mbar_init(&full[g][1], 1);
         mbar_fence_init();
     }
     pdl_wait();
-    if (tid == 0) {
+    if (lead) {
 #pragma unroll
         for (int s = 0; s < 2; ++s) {
-            const int tile = int(atomicAdd(a.tile_ctr, 1u));
-            tileq[s] = tile;
-            if (tile < ntiles) {
-                mbar_expect_tx(&full[s], TILE_BYTES);
-                bulk_g2s(fsm + s * SLOT, a.data + size_t(tile) * LINES * N, TILE_BYTES, &full[s]);
+            const int m = int(atomicAdd(a.tile_ctr, 1u));
+            lineq[g][s] = m;
+            if (m < nlines) {
+                if (a.debug & 2) {
+                    mbar_expect_tx(&full[g][s], 0);
+                } else {
+                    mbar_expect_tx(&full[g][s], LINE_BYTES);
+                    bulk_g2s(slots + s * SLOT, a.data + size_t(m) * N, LINE_BYTES, &full[g][s]);
+                }
             }
         }
     }
-    __syncthreads();
+    group_sync(bid, TF);
     for (int it = 0;; ++it) {
         const int s = it & 1;
-        const int tile = tileq[s];
-        if (tile >= ntiles) break;
+        const int m = lineq[g][s];
+        if (m >= nlines) break;
         unsigned next = 0;
-        if (tid == 0) next = atomicAdd(a.tile_ctr, 1u);
-        float2* buf = fsm + s * SLOT;
-        const int m = tile * LINES + li;
-        mbar_wait(&full[s], (it >> 1) & 1);
+        if (lead) next = atomicAdd(a.tile_ctr, 1u);
+        float2* line = slots + s * SLOT;
+        mbar_wait(&full[g][s], (it >> 1) & 1);
         cx<float> v[16];
-        const float2* src = buf + li * N + t;
 #pragma unroll
         for (int r = 0; r < 16; ++r) {
-            const float2 z = src[r * TF];
+            const float2 z = line[t + r * TF];
             v[r] = mk(z.x, z.y);
         }
-        float2* line = buf + li * LW;
-        fast_fft<N, TH, +1>(v, line, t, pt, tw);
+        if (a.debug != 1) fast_fft<N, TH, +1>(v, line, t, pt, tw, (a.debug & 4) ? -1 : bid, TF);
 #pragma unroll
         for (int r = 0; r < 16; ++r) {
             const float amp = a.beam ? __ldg(a.beam + size_t(m) * N + t + r * TF) : 1.0f;
@@ -237,22 +306,112 @@ __global__ void __launch_bounds__(TH, MINB) fast_row_holo(FastArgs a) {
                 v[r] = h;
             }
         }
-        fast_fft<N, TH, -1>(v, line, t, pt, tw);
+        if (a.debug != 1) fast_fft<N, TH, -1>(v, line, t, pt, tw, (a.debug & 4) ? -1 : bid, TF);
+        float2* dst = a.data + size_t(m) * N + t;
+        if (!(a.debug & 2)) {
+#pragma unroll
+            for (int r = 0; r < 16; ++r) dst[r * TF] = make_float2(v[r].x, v[r].y);
+        }
+        fence_proxy_async();
+        group_sync(bid, TF);
+        if (lead) {
+            const int nm = int(next);
+            lineq[g][s] = nm;
+            if (nm < nlines) {
+                if (a.debug & 2) {
+                    mbar_expect_tx(&full[g][s], 0);
+                } else {
+                    mbar_expect_tx(&full[g][s], LINE_BYTES);
+                    bulk_g2s(line, a.data + size_t(nm) * N, LINE_BYTES, &full[g][s]);
+                }
+            }
+        }
+        group_sync(bid, TF);
+    }
+    pdl_trigger();
+    __syncthreads();
+    finish_ctas(a.tile_ctr);
+}
+
+// Row pass, occupancy variant: twiddles from a shared table, one slot per
+// row group (latency hidden by more resident groups instead of a second slot).
+template <int N, int TH, int MINB>
+__global__ void __launch_bounds__(TH, MINB) fast_row_holo_s(FastArgs a) {
+    using S = FastShape<N, TH>;
+    constexpr int TF = S::TF, GROUPS = S::LINES, LW = S::LW;
+    constexpr int SLOT = (LW + 15) / 16 * 16;
+    constexpr uint32_t LINE_BYTES = uint32_t(N) * 8u;
+    static_assert(TF % 32 == 0, "row groups must be whole warps");
+    extern __shared__ __align__(128) float2 fsm[];
+    __shared__ __align__(8) uint64_t full[GROUPS];
+    __shared__ int lineq[GROUPS];
+    const int tid = threadIdx.x, g = tid / TF, t = tid - g * TF;
+    const bool lead = (t == 0);
+    const int pt = padc(t);
+    const int nlines = a.H;
+    const int bid = 1 + g;
+    float2* tab = fsm;
+    float2* line = fsm + TwTables<N, TH>::WORDS + g * SLOT;
+    TwTables<N, TH>::load(tab, a.tw_row);
+    if (lead) {
+        mbar_init(&full[g], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    pdl_wait();
+    if (lead) {
+        const int m = int(atomicAdd(a.tile_ctr, 1u));
+        lineq[g] = m;
+        if (m < nlines) {
+            mbar_expect_tx(&full[g], LINE_BYTES);
+            bulk_g2s(line, a.data + size_t(m) * N, LINE_BYTES, &full[g]);
+        }
+    }
+    group_sync(bid, TF);
+    for (int it = 0;; ++it) {
+        const int m = lineq[g];
+        if (m >= nlines) break;
+        unsigned next = 0;
+        if (lead) next = atomicAdd(a.tile_ctr, 1u);
+        mbar_wait(&full[g], it & 1);
+        cx<float> v[16];
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+            const float2 z = line[t + r * TF];
+            v[r] = mk(z.x, z.y);
+        }
+        fast_fft_s<N, TH, +1>(v, line, t, pt, tab, bid, TF);
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+            const float amp = a.beam ? __ldg(a.beam + size_t(m) * N + t + r * TF) : 1.0f;
+            const float m2 = v[r].x * v[r].x + v[r].y * v[r].y;
+            if (m2 > 0.0f) {
+                const float k = amp * rsqrtf(m2);
+                v[r] = mk(v[r].x * k, v[r].y * k);
+            } else {
+                cx<float> h = mk(amp, 0.0f);
+                if (a.q_row) h = cmul(h, cmul(a.q_row[m], a.q_col[t + r * TF]));
+                v[r] = h;
+            }
+        }
+        fast_fft_s<N, TH, -1>(v, line, t, pt, tab, bid, TF);
+        fence_proxy_async();
+        group_sync(bid, TF);
+        if (lead) {
+            const int nm = int(next);
+            lineq[g] = nm;
+            if (nm < nlines) {
+                mbar_expect_tx(&full[g], LINE_BYTES);
+                bulk_g2s(line, a.data + size_t(nm) * N, LINE_BYTES, &full[g]);
+            }
+        }
         float2* dst = a.data + size_t(m) * N + t;
 #pragma unroll
         for (int r = 0; r < 16; ++r) dst[r * TF] = make_float2(v[r].x, v[r].y);
-        fence_proxy_async();
-        __syncthreads();
-        if (tid == 0) {
-            const int nt = int(next);
-            tileq[s] = nt;
-            if (nt < ntiles) {
-                mbar_expect_tx(&full[s], TILE_BYTES);
-                bulk_g2s(buf, a.data + size_t(nt) * LINES * N, TILE_BYTES, &full[s]);
-            }
-        }
+        group_sync(bid, TF);
     }
     pdl_trigger();
+    __syncthreads();
     finish_ctas(a.tile_ctr);
 }
 
