@@ -331,6 +331,29 @@ def run_ours(args):
                              "frac": obytes / (avg / 1000.0) / 1e9 / peak, "algorithmic_bytes": obytes}}
         oplan.close()
 
+    # SA / DBS (C4: 1024^2 binary, seed 3): proposals/s and pixels/s, fp64 state
+    search = None
+    if not args.no_search:
+        from paper_2006_10509_b200.slm import SlmSpec, binary_phase
+
+        scfg = make_cfg(3 + rank, n=1024, kind="fourier", algorithm="sa")
+        scfg.slm = SlmSpec(1024, 1024, binary_phase())
+        scfg.proposals = 20000
+        splan = GenerationPlan(scfg, (1024, 1024), precision=_native.FP64, device=local)
+        splan.set_target(natural_target(1024))
+        splan.sa(proposals=300)
+        rs, _ = splan.sa()
+        rd, _ = splan.dbs(max_passes=1)
+        search = {"sa": {"metric": "SA proposals/s (1024x1024 binary, 20000 proposals, auto T0)",
+                         "value": rs.iterations_executed / (rs.device_ms / 1000.0), "unit": "proposals/s",
+                         "run_ms": rs.device_ms, "final_error": rs.final_error},
+                  "dbs": {"metric": "DBS pixels/s (1024x1024 binary, one raster pass)",
+                          "value": 1024 * 1024 / (rd.device_ms / 1000.0), "unit": "pixels/s", "run_ms": rd.device_ms,
+                          "final_error": rd.final_error},
+                  "cpu_reference": {"sa_proposals_per_s": "150-186 (BASELINE.md, survey container)",
+                                    "dbs_pixels_per_s": "116 (BASELINE.md, survey container)"}}
+        splan.close()
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline_gs()
@@ -344,7 +367,8 @@ def run_ours(args):
                            "global_batch": world, "parallelism": f"replicas x{world}",
                            "l2": "256 MB device write between timed steps (excluded from step time)"},
                 "gpu_launches": launches, "wall_s_timed": t_wall,
-                "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clk.summary(), "ospr": ospr}
+                "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clk.summary(), "ospr": ospr,
+                "search": search}
         print(json.dumps(line), flush=True)
     plan.close()
     if world > 1:
@@ -360,6 +384,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-ospr", action="store_true")
+    ap.add_argument("--no-search", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -84,6 +84,40 @@ class GenerationPlan:
                                              max(1, nsub), ctypes.byref(rep), None))
         return rep, (tk, tv)
 
+    def sa(self, seed=None, proposals=None):
+        """run_sa on the resident target (plan must be FP64)."""
+        cfg = self.cfg
+        sp = _native.SaParams()
+        sp.proposals = int(cfg.proposals if proposals is None else proposals)
+        t0 = cfg.initial_temperature
+        sp.initial_temperature = -1.0 if t0 is None else float(t0)
+        sp.cooling_factor = float(cfg.cooling_factor)
+        sp.init_mode = _init_code(cfg.init_mode)
+        sp.rng = _native.Pcg64State.from_bitgen(np.random.PCG64(cfg.seed if seed is None else seed))
+        rep = _native.Report()
+        cap = sp.proposals // max(1, sp.proposals // 1000) + 3
+        tk = np.zeros(cap, np.int64)
+        tv = np.zeros(cap, np.float64)
+        _native.check(self.lib.cgh_plan_sa(self.handle, ctypes.byref(sp), _native.ptr(tk), _native.ptr(tv), cap,
+                                           ctypes.byref(rep), None))
+        return rep, (tk, tv)
+
+    def dbs(self, seed=None, max_passes=None):
+        """run_dbs (raster order) on the resident target (plan must be FP64)."""
+        cfg = self.cfg
+        dp = _native.DbsParams()
+        dp.max_passes = int(cfg.max_passes if max_passes is None else max_passes)
+        dp.scan_random = 0
+        dp.init_mode = _init_code(cfg.init_mode)
+        dp.rng = _native.Pcg64State.from_bitgen(np.random.PCG64(cfg.seed if seed is None else seed))
+        rep = _native.Report()
+        cap = dp.max_passes + 3
+        tk = np.zeros(cap, np.int64)
+        tv = np.zeros(cap, np.float64)
+        _native.check(self.lib.cgh_plan_dbs(self.handle, ctypes.byref(dp), _native.ptr(tk), _native.ptr(tv), cap,
+                                            ctypes.byref(rep), None))
+        return rep, (tk, tv)
+
     def download_indices(self, frames=1):
         out = np.empty((frames,) + self.shape, self.idx_dtype)
         _native.check(self.lib.cgh_plan_download_idx(self.handle, _native.ptr(out), frames))
