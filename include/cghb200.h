@@ -214,6 +214,11 @@ int cgh_best_delta(int32_t device, const double *replay_m, const double *target_
                    const double *col_tw, const int32_t *mu, const int32_t *mv, int64_t count, int32_t h,
                    int32_t w, const double *deltas, int64_t levels, int64_t *best_index, double *best_change);
 
+/* ---- host: materialise states[indices] as complex128 (the returned
+ * hologram of every runner) with `threads` host threads (no GPU needed). */
+int cgh_expand_states(const void *idx, int32_t idx_bytes, int64_t count, const double *states, int32_t n_states,
+                      double *out, int32_t threads);
+
 /* ---- host-side numpy-stream emulation (no GPU needed) -----------------
  * Generator.permutation(n) of a PCG64 stream (algorithms.py:437-439). */
 int cgh_permutation(const cgh_pcg64 *rng, int64_t n, int64_t *out);

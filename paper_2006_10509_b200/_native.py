@@ -37,7 +37,7 @@ EXPORTS = (
     "cgh_plan_sa", "cgh_plan_dbs",
     "cgh_plan_download_idx", "cgh_plan_stream", "cgh_plan_sync", "cgh_plan_profile",
     "cgh_delta_error", "cgh_commit_update", "cgh_best_delta",
-    "cgh_permutation", "cgh_random_doubles",
+    "cgh_permutation", "cgh_random_doubles", "cgh_expand_states",
 )
 
 
@@ -153,6 +153,7 @@ def _declare(lib):
         "cgh_commit_update": ([i32, P, P, P, P, P, i64, i32, i32, f64, f64], ctypes.c_int),
         "cgh_best_delta": ([i32, P, P, P, P, P, P, i64, i32, i32, P, i64, pP(i64), pP(f64)], ctypes.c_int),
         "cgh_permutation": ([pP(Pcg64State), i64, P], ctypes.c_int),
+        "cgh_expand_states": ([P, i32, i64, P, i32, P, i32], ctypes.c_int),
         "cgh_random_doubles": ([i32, pP(Pcg64State), i64, i64, P], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
@@ -200,6 +201,21 @@ def require_device():
     if device_count() == 0:
         raise errors.BackendUnavailableError(
             "no CUDA device visible: the B200 path has no CPU fallback (" + last_error() + ")")
+
+
+def expand_states(idx, table):
+    """states[idx] as complex128 via the library's threaded host expansion."""
+    idx = np.ascontiguousarray(idx)
+    table = np.ascontiguousarray(table, dtype=np.complex128)
+    out = np.empty(idx.shape, dtype=np.complex128)
+    nb = 1 if idx.dtype == np.uint8 else 4
+    if nb == 4 and idx.dtype != np.int32:
+        idx = idx.astype(np.int32)
+    import os as _os
+
+    threads = min(16, len(_os.sched_getaffinity(0)) if hasattr(_os, "sched_getaffinity") else 8)
+    check(library().cgh_expand_states(ptr(idx), nb, idx.size, ptr(table), table.size, ptr(out), threads))
+    return out
 
 
 def c128(a):

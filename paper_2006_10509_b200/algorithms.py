@@ -18,6 +18,7 @@ of the state set. There is no CPU fallback.
 from __future__ import annotations
 
 import ctypes
+import threading
 import time
 from dataclasses import dataclass, field
 
@@ -209,6 +210,32 @@ def _trace(tk, tv, n):
     return [(int(tk[i]), float(tv[i])) for i in range(n)]
 
 
+_plans = threading.local()
+_MAX_PLANS = 4
+
+
+def _cached_plan(cfg, shape):
+    """Per-thread cache of device plans (stream, buffers, tables) keyed by
+    everything a plan bakes in; reentrant because each thread owns its plans."""
+    from .plan import GenerationPlan, plan_key
+
+    prec, dev = runner_precision(), current_device()
+    key = plan_key(cfg, shape, prec, dev)
+    cache = getattr(_plans, "d", None)
+    if cache is None:
+        cache = _plans.d = {}
+    plan = cache.get(key)
+    if plan is None:
+        if len(cache) >= _MAX_PLANS:
+            old = cache.pop(next(iter(cache)))
+            old.close()
+        plan = GenerationPlan(cfg, shape, precision=prec, device=dev)
+        cache[key] = plan
+    else:
+        cache[key] = cache.pop(key)   # most recently used last
+    return plan
+
+
 # --- Gerchberg-Saxton ---------------------------------------------------------
 
 
@@ -217,32 +244,18 @@ def run_gs(cfg, target, illumination=None, progress=None, cancel=None):
     start = time.perf_counter()
     target = np.asarray(target, dtype=np.complex128)
     _check_inputs(cfg, target, illumination)
-    init = _init_code(cfg.init_mode)
-    pb, keep = _problem(cfg, target)
-    mask = _mask_bytes(cfg, target)
-    lib = _native.library()
+    _init_code(cfg.init_mode)
+    pb, keep = _problem(cfg, target)      # validates the propagation spec
+    _mask_bytes(cfg, target)
+    _native.library()
     _native.require_device()
-    tgt = _native.c128(target)
-    ill = _illum(illumination)
-    gp = _native.GsParams()
-    gp.iterations = int(cfg.iterations)
-    gp.feedback_gain = float(cfg.feedback_gain)
-    gp.quantize_each_iteration = 1 if cfg.quantize_each_iteration else 0
-    gp.init_mode = init
-    gp.rng = _native.Pcg64State.from_bitgen(np.random.PCG64(cfg.seed))
-    idx = _index_plane(pb.n_states, target.shape)
-    cap = max(0, int(cfg.iterations)) + 1
-    tk = np.zeros(cap, np.int64)
-    tv = np.zeros(cap, np.float64)
-    rep = _native.Report()
-    hooks = _Hooks(progress, cancel)
-    st = lib.cgh_gs_run(ctypes.byref(pb), ctypes.byref(gp), _native.ptr(tgt), _native.ptr(mask), _native.ptr(ill),
-                        _native.ptr(idx), None, _native.ptr(tk), _native.ptr(tv), cap, ctypes.byref(rep),
-                        ctypes.byref(hooks.cb))
-    hooks.raise_pending()
-    _native.check(st)
+    plan = _cached_plan(cfg, target.shape)
+    plan.set_target(target, illumination, cfg=cfg)
+    hooks = _Hooks(progress, cancel) if (progress is not None or cancel is not None) else None
+    rep, (tk, tv) = plan.gs(cfg=cfg, hooks=hooks)
+    idx = plan.download_indices(1)[0]
     del keep
-    holo = states(cfg.slm.scheme)[idx]
+    holo = _native.expand_states(idx, states(cfg.slm.scheme))
     return holo, RunReport(
         error_trace=_trace(tk, tv, rep.trace_len),
         final_error=float(rep.final_error),
@@ -288,39 +301,25 @@ def run_ospr(cfg, target, illumination=None, progress=None, cancel=None):
     target = np.asarray(target, dtype=np.complex128)
     _check_inputs(cfg, target, illumination)
     pb, keep = _problem(cfg, target)
-    mask = _mask_bytes(cfg, target)
-    lib = _native.library()
+    _mask_bytes(cfg, target)
+    _native.library()
     _native.require_device()
-    tgt = _native.c128(target)
-    ill = _illum(illumination)
-    nsub = max(0, int(cfg.subframes))
-    streams = np.random.SeedSequence(cfg.seed).spawn(nsub)
-    frame_rng = (_native.Pcg64State * max(1, nsub))()
-    for i, s in enumerate(streams):
-        frame_rng[i] = _native.Pcg64State.from_bitgen(np.random.PCG64(s))
-    op = _native.OsprParams(nsub, ctypes.cast(frame_rng, ctypes.POINTER(_native.Pcg64State)))
-    idx = _index_plane(pb.n_states, target.shape, max(1, nsub))
-    cap = max(1, nsub)
-    tk = np.zeros(cap, np.int64)
-    tv = np.zeros(cap, np.float64)
-    rep = _native.Report()
-    hooks = _Hooks(progress, cancel)
-    st = lib.cgh_ospr_run(ctypes.byref(pb), ctypes.byref(op), _native.ptr(tgt), _native.ptr(mask), _native.ptr(ill),
-                          _native.ptr(idx), _native.ptr(tk), _native.ptr(tv), cap, ctypes.byref(rep),
-                          ctypes.byref(hooks.cb))
-    hooks.raise_pending()
-    _native.check(st)
+    plan = _cached_plan(cfg, target.shape)
+    plan.set_target(target, illumination, cfg=cfg)
+    hooks = _Hooks(progress, cancel) if (progress is not None or cancel is not None) else None
+    rep, (tk, tv) = plan.ospr(cfg=cfg, hooks=hooks)
+    n = int(rep.iterations_executed)
+    frames = []
+    if n:
+        idx = plan.download_indices(n)
+        table = states(cfg.slm.scheme)
+        frames = [_native.expand_states(idx[i], table) for i in range(n)]
     del keep
-    table = states(cfg.slm.scheme)
-    frames = [table[idx[i]] for i in range(int(rep.iterations_executed))]
-    trace = _trace(tk, tv, rep.trace_len)
-    if rep.iterations_executed == 0 and progress is not None:
-        pass
     return frames, RunReport(
-        error_trace=trace,
+        error_trace=_trace(tk, tv, rep.trace_len),
         final_error=float(rep.final_error),
         efficiency=float(rep.efficiency),
-        iterations_executed=int(rep.iterations_executed),
+        iterations_executed=n,
         runtime_ms=_elapsed_ms(start),
         seed_used=cfg.seed,
         termination=_TERMINATION[rep.termination],

@@ -1,7 +1,9 @@
 // Host runtime + C-ABI for transforms, GS and OSPR (include/cghb200.h).
 #include <algorithm>
 #include <cmath>
+#include <atomic>
 #include <mutex>
+#include <thread>
 
 #include "runtime.cuh"
 
@@ -921,6 +923,35 @@ int cgh_ospr_run(const cgh_problem* pb, const cgh_ospr_params* op, const double*
     CGH_TRY(cgh_plan_ospr(P, op, trace_k, trace_v, trace_cap, &r, cb));
     if (rep) *rep = r;
     if (out_idx && r.iterations_executed > 0) CGH_TRY(cgh_plan_download_idx(P, out_idx, r.iterations_executed));
+    return CGH_OK;
+}
+
+int cgh_expand_states(const void* idx, int32_t idx_bytes, int64_t count, const double* states, int32_t n_states,
+                      double* out, int32_t threads) {
+    if (count < 0 || (count > 0 && (!idx || !states || !out)) || (idx_bytes != 1 && idx_bytes != 4))
+        return fail(CGH_ERR_VALUE, "bad arguments");
+    const int nt = std::max(1, std::min(threads > 0 ? threads : 8, 64));
+    std::vector<std::thread> pool;
+    std::atomic<int> bad{0};
+    auto work = [&](int64_t a, int64_t b) {
+        for (int64_t i = a; i < b; ++i) {
+            const int k = idx_bytes == 1 ? int(static_cast<const uint8_t*>(idx)[i]) : static_cast<const int32_t*>(idx)[i];
+            if (k < 0 || k >= n_states) {
+                bad = 1;
+                continue;
+            }
+            out[2 * i] = states[2 * k];
+            out[2 * i + 1] = states[2 * k + 1];
+        }
+    };
+    const int64_t chunk = (count + nt - 1) / nt;
+    for (int t = 1; t < nt; ++t) {
+        const int64_t a = t * chunk, b = std::min(count, a + chunk);
+        if (a < b) pool.emplace_back(work, a, b);
+    }
+    work(0, std::min(count, chunk));
+    for (auto& th : pool) th.join();
+    if (bad) return fail(CGH_ERR_VALUE, "index outside the state table");
     return CGH_OK;
 }
 

@@ -19,6 +19,17 @@ PASS_NAMES = {0: "row_fwd", 1: "row_inv", 2: "row_holo", 3: "row_init", 4: "ospr
               8: "col_fwd", 9: "col_inv", 10: "col_gs", 11: "col_final", 12: "col_holo"}
 
 
+def plan_key(cfg, shape, precision, device):
+    """Everything a plan bakes in: shape, precision, device, state table,
+    propagation parameters, rescale flag."""
+    from .slm import states
+
+    p = cfg.propagation
+    return (tuple(shape), int(precision), int(device), states(cfg.slm.scheme).tobytes(),
+            float(getattr(cfg.slm.scheme, "phase_offset", 0.0)), p.kind, float(p.wavelength), float(p.distance),
+            float(p.pitch_x), float(p.pitch_y), bool(cfg.metric.rescale))
+
+
 class GenerationPlan:
     def __init__(self, cfg, shape, precision=None, device=None):
         self.lib = _native.library()
@@ -46,15 +57,15 @@ class GenerationPlan:
         except Exception:  # noqa: BLE001
             pass
 
-    def set_target(self, target, illumination=None):
+    def set_target(self, target, illumination=None, cfg=None):
         target = _native.c128(target)
-        mask = _mask_bytes(self.cfg, target)
+        mask = _mask_bytes(cfg or self.cfg, target)
         ill = None if illumination is None else _native.c128(illumination)
         _native.check(self.lib.cgh_plan_set_target(self.handle, _native.ptr(target), _native.ptr(mask),
                                                    _native.ptr(ill)))
 
-    def gs(self, seed=None, iterations=None, with_trace=True):
-        cfg = self.cfg
+    def gs(self, seed=None, iterations=None, with_trace=True, cfg=None, hooks=None):
+        cfg = cfg or self.cfg
         gp = _native.GsParams()
         gp.iterations = int(cfg.iterations if iterations is None else iterations)
         gp.feedback_gain = float(cfg.feedback_gain)
@@ -65,12 +76,16 @@ class GenerationPlan:
         cap = gp.iterations + 1
         tk = np.zeros(cap, np.int64) if with_trace else None
         tv = np.zeros(cap, np.float64) if with_trace else None
-        _native.check(self.lib.cgh_plan_gs(self.handle, ctypes.byref(gp), _native.ptr(tk), _native.ptr(tv),
-                                           cap if with_trace else 0, ctypes.byref(rep), None))
+        st = self.lib.cgh_plan_gs(self.handle, ctypes.byref(gp), _native.ptr(tk), _native.ptr(tv),
+                                  cap if with_trace else 0, ctypes.byref(rep),
+                                  None if hooks is None else ctypes.byref(hooks.cb))
+        if hooks is not None:
+            hooks.raise_pending()
+        _native.check(st)
         return rep, (tk, tv)
 
-    def ospr(self, seed=None, subframes=None):
-        cfg = self.cfg
+    def ospr(self, seed=None, subframes=None, cfg=None, hooks=None):
+        cfg = cfg or self.cfg
         nsub = int(cfg.subframes if subframes is None else subframes)
         streams = np.random.SeedSequence(cfg.seed if seed is None else seed).spawn(nsub)
         fr = (_native.Pcg64State * max(1, nsub))()
@@ -80,8 +95,12 @@ class GenerationPlan:
         rep = _native.Report()
         tk = np.zeros(max(1, nsub), np.int64)
         tv = np.zeros(max(1, nsub), np.float64)
-        _native.check(self.lib.cgh_plan_ospr(self.handle, ctypes.byref(op), _native.ptr(tk), _native.ptr(tv),
-                                             max(1, nsub), ctypes.byref(rep), None))
+        st = self.lib.cgh_plan_ospr(self.handle, ctypes.byref(op), _native.ptr(tk), _native.ptr(tv),
+                                    max(1, nsub), ctypes.byref(rep),
+                                    None if hooks is None else ctypes.byref(hooks.cb))
+        if hooks is not None:
+            hooks.raise_pending()
+        _native.check(st)
         return rep, (tk, tv)
 
     def sa(self, seed=None, proposals=None):
