@@ -75,6 +75,29 @@ struct Bcast {
 };
 
 // ---------------------------------------------------------------- SA
+// A proposal drawn by thread 0 ahead of time (algorithms.py:334-340):
+// pixel, raw level draw, stream state after the draws, prefetched index.
+struct Draw {
+    Pcg64 g;
+    int m, n, jraw, idx;
+};
+
+__device__ __forceinline__ void draw_ahead(const SearchArgs& a, Pcg64 g, Draw& d) {
+    const uint32_t p = pcg_integers(g, uint64_t(a.H) * uint64_t(a.W));
+    d.m = int(p >> a.logW);
+    d.n = int(p & (a.W - 1));
+    d.jraw = int(pcg_integers(g, uint64_t(a.L - 1)));
+    d.g = g;
+    d.idx = read_index(a, (long long)d.m * a.W + d.n);   // consumed after the grid barrier
+}
+
+__device__ __forceinline__ double2 level_delta_s(const SearchArgs& a, const double2* st_s, int m, int n, int j, int cur) {
+    const double2 sj = a.L <= 64 ? st_s[j] : a.states[j], sc = a.L <= 64 ? st_s[cur] : a.states[cur];
+    double2 d = make_double2(sj.x - sc.x, sj.y - sc.y);
+    if (a.qr) d = dmul(d, dmul(a.qr[m], a.qc[n]));
+    return d;
+}
+
 __global__ void __launch_bounds__(kSearchThreads, 1) sa_kernel(SearchArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     SmemLayout L;
@@ -82,10 +105,18 @@ __global__ void __launch_bounds__(kSearchThreads, 1) sa_kernel(SearchArgs a) {
     __shared__ Bcast bc;
     __shared__ SearchState st;
     __shared__ double red[8];
+    __shared__ double2 st_s[64];
+    if (threadIdx.x < 64 && threadIdx.x < a.L) st_s[threadIdx.x] = a.states[threadIdx.x];
     if (threadIdx.x == 0) st = *a.st;
     __syncthreads();
     unsigned long long phase = st.bar / gridDim.x;
     const bool lead = (blockIdx.x == 0 && threadIdx.x == 0);
+    // thread 0 state: the next proposal for both outcomes of the Metropolis draw
+    Draw nxA, nxB;
+    Pcg64 g_after_u;
+    double u_next = 0.0;
+    bool have_next = false;
+    int c1_m = -1, c1_n = -1, c1_j = 0;   // commit of the previous proposal (may not be visible yet)
     for (;;) {
         if (threadIdx.x == 0) {
             bc.pend = st.pend;
@@ -96,16 +127,18 @@ __global__ void __launch_bounds__(kSearchThreads, 1) sa_kernel(SearchArgs a) {
             const bool warm = st.warm_left > 0;
             bc.go = warm || st.executed < a.k_end;
             if (bc.go) {
-                // _draw_proposal (algorithms.py:334-340)
-                const uint32_t p = pcg_integers(st.rng, uint64_t(a.H) * uint64_t(a.W));
-                const int m = int(p >> a.logW), n = int(p & (a.W - 1));
-                int j = int(pcg_integers(st.rng, uint64_t(a.L - 1)));
-                int cur = read_index(a, (long long)m * a.W + n);
-                if (st.pend && st.pend_m == m && st.pend_n == n) cur = st.pend_j;   // commit not yet visible
+                Draw cur_d;
+                if (!have_next) draw_ahead(a, st.rng, cur_d);
+                else cur_d = nxA;   // branch chosen at the last decision is stored in nxA
+                st.rng = cur_d.g;
+                int cur = cur_d.idx;
+                if (st.pend && st.pend_m == cur_d.m && st.pend_n == cur_d.n) cur = st.pend_j;   // commit k-1
+                else if (c1_m == cur_d.m && c1_n == cur_d.n) cur = c1_j;                      // commit k-2
+                int j = cur_d.jraw;
                 if (j >= cur) j += 1;
-                const double2 d = level_delta(a, m, n, j, cur);
-                bc.m = m;
-                bc.n = n;
+                const double2 d = level_delta_s(a, st_s, cur_d.m, cur_d.n, j, cur);
+                bc.m = cur_d.m;
+                bc.n = cur_d.n;
                 bc.j = j;
                 bc.cur = cur;
                 bc.dre = d.x;
@@ -114,6 +147,15 @@ __global__ void __launch_bounds__(kSearchThreads, 1) sa_kernel(SearchArgs a) {
         }
         __syncthreads();
         if (!bc.go) break;
+        if (threadIdx.x == 0) {
+            // draw proposal k+1 for both outcomes while the sweep and barrier run
+            draw_ahead(a, st.rng, nxA);
+            Pcg64 gb = st.rng;
+            u_next = pcg_next_double(gb);
+            g_after_u = gb;
+            draw_ahead(a, gb, nxB);
+            have_next = true;
+        }
         const int m = bc.m, n = bc.n, pm = bc.pm, pn = bc.pn;
         const double2 d = make_double2(bc.dre, bc.dim), pd = make_double2(bc.pre, bc.pim);
         const bool pend = bc.pend != 0;
@@ -138,7 +180,16 @@ __global__ void __launch_bounds__(kSearchThreads, 1) sa_kernel(SearchArgs a) {
         grid_reduce(a, acc, 1, phase, red);
         if (threadIdx.x == 0) {
             const double change = red[0];
+            // the commit applied in this sweep (k-1) becomes "k-2" for the next draw
+            if (st.pend) {
+                c1_m = st.pend_m;
+                c1_n = st.pend_n;
+                c1_j = st.pend_j;
+            } else {
+                c1_m = -1;
+            }
             st.pend = 0;
+            bool drew = false;
             if (st.warm_left > 0) {
                 st.warm_total += fabs(change) / a.denom;
                 st.warm_left -= 1;
@@ -146,7 +197,10 @@ __global__ void __launch_bounds__(kSearchThreads, 1) sa_kernel(SearchArgs a) {
             } else {
                 const double x = change / a.denom;
                 bool ok = x < 0.0;
-                if (!ok && st.temperature > 0.0) ok = pcg_next_double(st.rng) < exp(-x / st.temperature);
+                if (!ok && st.temperature > 0.0) {
+                    drew = true;   // rng.random() (algorithms.py:388-389)
+                    ok = u_next < exp(-x / st.temperature);
+                }
                 if (ok) {
                     st.error_num += change;
                     st.pend = 1;
@@ -171,10 +225,16 @@ __global__ void __launch_bounds__(kSearchThreads, 1) sa_kernel(SearchArgs a) {
                     *a.trace_len = c + 1;
                 }
             }
+            if (drew) {
+                st.rng = g_after_u;   // the Metropolis draw is consumed
+                nxA = nxB;            // and the next proposal follows it
+            }
+            // st.rng is replaced by the chosen draw's stream state at the top
         }
         __syncthreads();
     }
-    // apply the last accepted commit so the stored replay is current
+    // the stream state to persist: proposals drawn ahead are not consumed
+    // (st.rng holds the state after the last consumed draws)
     if (st.pend) {
         const double2 pd = make_double2(st.pend_re, st.pend_im);
         for (long long li = threadIdx.x; li < s.count; li += blockDim.x) {

@@ -139,10 +139,15 @@ __device__ __forceinline__ void grid_reduce(const SearchArgs& a, double* vals, i
     if (threadIdx.x < nq) buf[(size_t)blockIdx.x * nq + threadIdx.x] = vals[threadIdx.x];
     phase += 1;
     grid_sync(&a.st->bar, phase * (unsigned long long)G);
-    for (int q = threadIdx.x; q < nq; q += blockDim.x) {
+    // warp w reduces quantities q = w, w + nwarps, ...: lane l sums CTAs
+    // l, l+32, ... (independent loads), then a fixed shuffle tree
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int q = warp; q < nq; q += nw) {
         double s = 0;
-        for (int b = 0; b < G; ++b) s += __ldcg(&buf[(size_t)b * nq + q]);
-        sh_out[q] = s;
+        for (int b = lane; b < G; b += 32) s += __ldcg(&buf[(size_t)b * nq + q]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) sh_out[q] = s;
     }
     __syncthreads();
 }
