@@ -10,7 +10,10 @@ struct FastState {
     CUtensorMap tmap;           // data as float32 [H][2W], box {2C, 256}
     const void* tmap_ptr = nullptr;
     int H = 0, W = 0;
-    DevBuf tgt_tiled, ctr;
+    CUtensorMap tmap_frames;    // OSPR frames stacked: float32 [F*H][2W]
+    const void* tmapf_ptr = nullptr;
+    int tmapf_rows = 0;
+    DevBuf tgt_tiled, ctr, line_state, line_part;
     const void* tgt_src = nullptr;
 };
 
@@ -64,6 +67,8 @@ void fast_free(cgh_plan* P) {
     FastState* F = static_cast<FastState*>(P->fast);
     if (!F) return;
     if (F->tgt_tiled.p) cudaFreeAsync(F->tgt_tiled.p, P->st);
+    if (F->line_state.p) cudaFreeAsync(F->line_state.p, P->st);
+    if (F->line_part.p) cudaFreeAsync(F->line_part.p, P->st);
     if (F->ctr.p) cudaFreeAsync(F->ctr.p, P->st);
     delete F;
     P->fast = nullptr;
@@ -226,6 +231,200 @@ static cudaError_t col_launch(cgh_plan* P, const FastArgs& f) {
     const int mode = (P->rescale ? 1 : 0) | (f.gain != 0.0f ? 2 : 0);
     if (col_th() == 256) return col_launch_th<N, 256, 2>(P, f, mode);
     return col_launch_th<N, 512, 1>(P, f, mode);
+}
+
+static int encode_2d(CUtensorMap* m, void* ptr, int W, int rows, int C, int box_rows) {
+    cuuint64_t dims[2] = {cuuint64_t(2) * W, cuuint64_t(rows)};
+    cuuint64_t strides[1] = {cuuint64_t(W) * 8};
+    cuuint32_t box[2] = {cuuint32_t(2 * C), cuuint32_t(box_rows)};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, ptr, dims, strides, box, estr,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(CGH_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", int(r));
+    return CGH_OK;
+}
+
+bool fast_ospr_eligible(cgh_plan* P) {
+    if (P->prec != CGH_FP32 || P->idx_bytes != 1) return false;
+    const int lc = fast_lines_th(P->H, 512);
+    if (lc < 1 || P->W < lc || P->H < 512 || P->W < 512 || P->W > 4096) return false;
+    if (getenv("CGHB200_NO_FAST")) return false;
+    return encode_fn() != nullptr;
+}
+
+template <int N>
+static cudaError_t holo_launch(cgh_plan* P, const FastHoloArgs& h, const CUtensorMap& map) {
+    using S = FastShape<N, 512>;
+    const size_t smem = size_t(2) * ((S::LINES * S::LW + 15) / 16 * 16) * sizeof(float2);
+    auto k = fast_col_holo<N, 512, 1>;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        attr = true;
+    }
+    const int tiles = h.frames * (P->W / S::LINES);
+    const int grid = std::max(1, std::min(sm_count(P->dev), tiles));
+    return launch_pdl(k, grid, 512, smem, P->st, h, map);
+}
+
+// OSPR K2 over `frames` stacked frames in the data buffer (capacity `cap` frames).
+int fast_ospr_holo(cgh_plan* P, const PassArgs<float>& a, int frames, int cap, uint8_t* idx_out) {
+    FastState* F = static_cast<FastState*>(P->fast);
+    if (!F) {
+        F = new FastState();
+        P->fast = F;
+    }
+    if (!F->ctr.p) {
+        CGH_TRY(ensure(P, F->ctr, 64));
+        CGH_CUDA(cudaMemsetAsync(F->ctr.p, 0, 64, P->st));
+    }
+    const int C = fast_lines_th(P->H, 512);
+    if (F->tmapf_ptr != P->data.p || F->tmapf_rows != cap * P->H) {
+        CGH_TRY(encode_2d(&F->tmap_frames, P->data.p, P->W, cap * P->H, C, std::min(kFastBoxRows, P->H)));
+        F->tmapf_ptr = P->data.p;
+        F->tmapf_rows = cap * P->H;
+    }
+    FastHoloArgs h;
+    h.data = reinterpret_cast<float2*>(a.data);
+    h.H = P->H;
+    h.W = P->W;
+    h.frames = frames;
+    h.beam = a.beam;
+    h.tw_col = a.tw_col;
+    h.q_row = a.q_row;
+    h.q_col = a.q_col;
+    h.scheme = a.scheme;
+    h.idx = idx_out;
+    h.binary = (P->scheme_kind == CGH_SCHEME_PHASE && P->nstates == 2 && P->offset == 0.0) ? 1 : 0;
+    h.tile_ctr = static_cast<unsigned*>(F->ctr.p);
+    if (P->profiling) CGH_TRY(prof_mark(P, 8 + COL_HOLO, true));
+    cudaError_t e;
+    switch (P->H) {
+        case 512: e = holo_launch<512>(P, h, F->tmap_frames); break;
+        case 1024: e = holo_launch<1024>(P, h, F->tmap_frames); break;
+        case 2048: e = holo_launch<2048>(P, h, F->tmap_frames); break;
+        case 4096: e = holo_launch<4096>(P, h, F->tmap_frames); break;
+        default: return fail(CGH_ERR_UNSUPPORTED, "fast OSPR column pass H=%d", P->H);
+    }
+    if (P->profiling) CGH_TRY(prof_mark(P, 8 + COL_HOLO, false));
+    P->launches += 1;
+    if (e != cudaSuccess) return fail(CGH_ERR_CUDA, "fast OSPR column pass: %s", cudaGetErrorString(e));
+    return CGH_OK;
+}
+
+// ---- OSPR K1 / K3 ----------------------------------------------------------
+constexpr int kOsprTH = 256, kOsprMinB = 2;
+
+template <int N>
+static cudaError_t gen_launch(cgh_plan* P, const FastOsprArgs& o) {
+    using S = FastShape<N, kOsprTH>;
+    const size_t smem = size_t(S::LINES) * ((S::LW + 15) / 16 * 16) * sizeof(float2);
+    auto k = fast_ospr_gen<N, kOsprTH, kOsprMinB>;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        attr = true;
+    }
+    const int grid = std::max(1, std::min(kOsprMinB * sm_count(P->dev), (o.frames * o.H + S::LINES - 1) / S::LINES));
+    return launch_pdl(k, grid, kOsprTH, smem, P->st, o);
+}
+
+template <int N>
+static cudaError_t acc_launch(cgh_plan* P, const FastOsprArgs& o) {
+    using S = FastShape<N, kOsprTH>;
+    const size_t smem = (size_t(TwTables<N, kOsprTH>::WORDS) + size_t(S::LINES) * 2 * ((S::LW + 15) / 16 * 16)) * sizeof(float2);
+    auto k = fast_ospr_acc<N, kOsprTH, kOsprMinB>;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        attr = true;
+    }
+    const int grid = std::max(1, std::min(kOsprMinB * sm_count(P->dev), (o.H + S::LINES - 1) / S::LINES));
+    return launch_pdl(k, grid, kOsprTH, smem, P->st, o);
+}
+
+static int fast_ospr_common(cgh_plan* P, const PassArgs<float>& a, FastOsprArgs& o) {
+    FastState* F = static_cast<FastState*>(P->fast);
+    if (!F) {
+        F = new FastState();
+        P->fast = F;
+    }
+    if (!F->ctr.p) {
+        CGH_TRY(ensure(P, F->ctr, 64));
+        CGH_CUDA(cudaMemsetAsync(F->ctr.p, 0, 64, P->st));
+    }
+    o.data = reinterpret_cast<float2*>(a.data);
+    o.H = P->H;
+    o.W = P->W;
+    o.frames = a.frames;
+    o.frame0 = a.frame0;
+    o.nframes_total = a.nframes_total;
+    o.tgt = a.tgt;
+    o.tw_row = a.tw_row;
+    o.scale = a.scale;
+    o.intensity = a.intensity;
+    o.load_intensity = a.load_intensity;
+    o.store_intensity = a.store_intensity;
+    o.tile_ctr = static_cast<unsigned*>(F->ctr.p);
+    return CGH_OK;
+}
+
+// K1: line start states + random-phase rows + inverse row FFT
+int fast_ospr_gen(cgh_plan* P, const PassArgs<float>& a) {
+    FastOsprArgs o;
+    CGH_TRY(fast_ospr_common(P, a, o));
+    FastState* F = static_cast<FastState*>(P->fast);
+    const int lines = a.frames * P->H;
+    CGH_TRY(ensure(P, F->line_state, sizeof(Pcg64) * size_t(std::max(lines, 1))));
+    ospr_line_states<<<(lines + 255) / 256, 256, 0, P->st>>>(a.frame_rng, a.frame0, a.frames, P->H, P->W,
+                                                            static_cast<Pcg64*>(F->line_state.p));
+    P->launches += 1;
+    CGH_CUDA(cudaGetLastError());
+    o.line_state = static_cast<const Pcg64*>(F->line_state.p);
+    if (P->profiling) CGH_TRY(prof_mark(P, ROW_OSPR_GEN, true));
+    cudaError_t e;
+    switch (P->W) {
+        case 512: e = gen_launch<512>(P, o); break;
+        case 1024: e = gen_launch<1024>(P, o); break;
+        case 2048: e = gen_launch<2048>(P, o); break;
+        case 4096: e = gen_launch<4096>(P, o); break;
+        default: return fail(CGH_ERR_UNSUPPORTED, "fast OSPR row pass W=%d", P->W);
+    }
+    if (P->profiling) CGH_TRY(prof_mark(P, ROW_OSPR_GEN, false));
+    P->launches += 1;
+    if (e != cudaSuccess) return fail(CGH_ERR_CUDA, "fast OSPR generation: %s", cudaGetErrorString(e));
+    return CGH_OK;
+}
+
+// K3: forward rows, intensity accumulation, per-line partials, fixed-order totals
+int fast_ospr_acc(cgh_plan* P, const PassArgs<float>& a) {
+    FastOsprArgs o;
+    CGH_TRY(fast_ospr_common(P, a, o));
+    FastState* F = static_cast<FastState*>(P->fast);
+    const bool tail = (a.frame0 + a.frames == a.nframes_total);
+    const size_t nq = size_t(3 * a.frames + 2);
+    CGH_TRY(ensure(P, F->line_part, sizeof(double) * nq * P->H));
+    o.line_part = static_cast<double*>(F->line_part.p);
+    if (P->profiling) CGH_TRY(prof_mark(P, ROW_OSPR_ACC, true));
+    cudaError_t e;
+    switch (P->W) {
+        case 512: e = acc_launch<512>(P, o); break;
+        case 1024: e = acc_launch<1024>(P, o); break;
+        case 2048: e = acc_launch<2048>(P, o); break;
+        case 4096: e = acc_launch<4096>(P, o); break;
+        default: return fail(CGH_ERR_UNSUPPORTED, "fast OSPR accumulation W=%d", P->W);
+    }
+    if (e == cudaSuccess) {
+        ospr_line_reduce<<<a.frames + (tail ? 1 : 0), 256, 0, P->st>>>(
+            static_cast<const double*>(F->line_part.p), P->H, a.frames, a.frame0, tail ? 1 : 0, a.nframes_total,
+            a.red.denom, a.red.rescale, a.red.out);
+        e = cudaGetLastError();
+    }
+    if (P->profiling) CGH_TRY(prof_mark(P, ROW_OSPR_ACC, false));
+    P->launches += 2;
+    if (e != cudaSuccess) return fail(CGH_ERR_CUDA, "fast OSPR accumulation: %s", cudaGetErrorString(e));
+    return CGH_OK;
 }
 
 int fast_row(cgh_plan* P, const PassArgs<float>& a) {

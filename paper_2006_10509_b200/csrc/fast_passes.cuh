@@ -457,8 +457,8 @@ __global__ void __launch_bounds__(TH, MINB) fast_col_gs(FastArgs a, const __grid
         }
     }
     __syncthreads();
-    float sdd = 0.f, srr = 0.f, srd = 0.f;
     const float gain = a.gain;
+    const double sc2 = double(a.scale) * double(a.scale);
     for (int it = 0;; ++it) {
         const int s = it & 1;
         const int tile = tileq[s];
@@ -477,6 +477,7 @@ __global__ void __launch_bounds__(TH, MINB) fast_col_gs(FastArgs a, const __grid
         }
         float2* line = buf + c * LW;
         fast_fft<N, TH, -1>(v, line, t, pt, tw);
+        float sdd = 0.f, srr = 0.f, srd = 0.f;
 #pragma unroll
         for (int r = 0; r < 16; ++r) {
             const float x = v[r].x, y = v[r].y;
@@ -497,6 +498,17 @@ __global__ void __launch_bounds__(TH, MINB) fast_col_gs(FastArgs a, const __grid
             const float k = in ? (pos ? want * ri : 0.0f) : 1.0f;
             v[r] = mk(x * k + ((in && !pos) ? want : 0.0f), y * k);
         }
+        // per-tile sums -> global slot of this tile (fixed-order total at the end,
+        // independent of which CTA claimed which tile)
+        {
+            double ts[3] = {double(sdd), double(srr), double(srd)};
+            block_reduce<3>(ts, rsh);
+            if (tid == 0) {
+                a.red.partials[3 * size_t(tile) + 0] = ts[0] * sc2;
+                a.red.partials[3 * size_t(tile) + 1] = ts[1] * sc2;
+                a.red.partials[3 * size_t(tile) + 2] = ts[2] * sc2;
+            }
+        }
         fast_fft<N, TH, +1>(v, line, t, pt, tw);
         float2* dst = a.data + size_t(tile) * C + c + size_t(t) * a.W;
         const size_t step = size_t(TF) * a.W;
@@ -511,22 +523,418 @@ __global__ void __launch_bounds__(TH, MINB) fast_col_gs(FastArgs a, const __grid
         }
     }
     pdl_trigger();
-    // sums in units of the unscaled transform: multiply by scale^2 once
-    const double sc2 = double(a.scale) * double(a.scale);
-    double acc[4] = {double(sdd) * sc2, double(srr) * sc2, double(srd) * sc2, 0.0};
-    block_reduce<4>(acc, rsh);
-    const int nblocks = gridDim.x;
-    if (publish_partials<4>(a.red, acc, nblocks, blockIdx.x)) {
-        const double s_dd = sum_partials(a.red, 0, nblocks, rsh);
-        const double s_rr = sum_partials(a.red, 1, nblocks, rsh);
-        const double s_rd = sum_partials(a.red, 2, nblocks, rsh);
-        if (threadIdx.x == 0) {
-            a.red.out[0] = error_from_sums(s_dd, s_rr, s_rd, *a.red.denom, RESCALE ? a.red.rescale : 0);
+    __shared__ int last;
+    __syncthreads();
+    if (tid == 0) {
+        __threadfence();
+        last = (atomicAdd(a.red.counter, 1u) == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (last) {
+        __threadfence();
+        const int lane = tid & 31, warp = tid >> 5;
+        if (warp < 3) {
+            double v = 0;
+            for (int b = lane; b < ntiles; b += 32) v += __ldcg(&a.red.partials[3 * size_t(b) + warp]);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (lane == 0) rsh[warp] = v;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            a.red.out[0] = error_from_sums(rsh[0], rsh[1], rsh[2], *a.red.denom, RESCALE ? a.red.rescale : 0);
             a.red.out[1] = 0.0;   // efficiency is reported by the final (generic) pass only
             *a.red.counter = 0u;
             a.tile_ctr[0] = 0u;
             a.tile_ctr[1] = 0u;
         }
+    }
+}
+
+// ====================================================== OSPR hologram columns
+// K2 of OSPR (algorithms.py:500-503): per (subframe, column tile): inverse
+// column FFT -> x conj(q) -> beam x/|x| -> snap (index plane) -> state q ->
+// forward column FFT. Frames are stacked vertically in one tensor map.
+struct FastHoloArgs {
+    float2* data;                 // frames x H x W complex64
+    int H, W, frames;
+    const float* beam;
+    const cx<float>* tw_col;
+    const cx<float>* q_row;       // Fresnel factors or nullptr
+    const cx<float>* q_col;
+    SchemeDev scheme;
+    uint8_t* idx;                 // frames x H x W, index planes (uint8 only)
+    int binary;                   // PhaseOnly(2, offset 0): snap by the sign of Re
+    unsigned* tile_ctr;
+};
+
+template <int N, int TH, int MINB>
+__global__ void __launch_bounds__(TH, MINB) fast_col_holo(FastHoloArgs a, const __grid_constant__ CUtensorMap tmap) {
+    using S = FastShape<N, TH>;
+    constexpr int TF = S::TF, C = S::LINES, LW = S::LW;
+    constexpr int SLOT = (C * LW + 15) / 16 * 16;
+    constexpr uint32_t TILE_BYTES = uint32_t(C) * N * 8u;
+    extern __shared__ __align__(128) float2 fsm[];
+    __shared__ __align__(8) uint64_t full[2];
+    __shared__ int tileq[2];
+    const int tid = threadIdx.x, t = tid / C, c = tid - t * C;
+    const int pt = padc(t);
+    const int cgroups = a.W / C;
+    const int ntiles = a.frames * cgroups;
+    FastTw<N, TH> tw;
+    fast_tw_init<N, TH>(tw, t, a.tw_col);
+    auto issue = [&](int s, int tile) {
+        const int f = tile / cgroups, cg = tile - f * cgroups;
+        mbar_expect_tx(&full[s], TILE_BYTES);
+#pragma unroll 1
+        for (int y = 0; y < N; y += kFastBoxRows)
+            tma_g2s_2d(fsm + s * SLOT + y * C, &tmap, 2 * cg * C, f * N + y, &full[s]);
+    };
+    if (tid == 0) {
+        mbar_init(&full[0], 1);
+        mbar_init(&full[1], 1);
+        mbar_fence_init();
+    }
+    pdl_wait();
+    if (tid == 0) {
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+            const int tile = int(atomicAdd(a.tile_ctr, 1u));
+            tileq[s] = tile;
+            if (tile < ntiles) issue(s, tile);
+        }
+    }
+    __syncthreads();
+    const bool fres = a.q_row != nullptr;
+    for (int it = 0;; ++it) {
+        const int s = it & 1;
+        const int tile = tileq[s];
+        if (tile >= ntiles) break;
+        unsigned next = 0;
+        if (tid == 0) next = atomicAdd(a.tile_ctr, 1u);
+        const int f = tile / cgroups, cg = tile - f * cgroups;
+        const int n = cg * C + c;
+        float2* buf = fsm + s * SLOT;
+        mbar_wait(&full[s], (it >> 1) & 1);
+        cx<float> v[16];
+        const float2* src = buf + t * C + c;
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+            const float2 z = src[r * TF * C];
+            v[r] = mk(z.x, z.y);
+        }
+        float2* line = buf + c * LW;
+        fast_fft<N, TH, +1>(v, line, t, pt, tw);
+        const cx<float> qn = fres ? a.q_col[n] : mk(1.0f, 0.0f);
+        uint8_t* ip = a.idx + size_t(f) * N * a.W + n;
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+            const int m = t + r * TF;
+            cx<float> x = v[r];
+            cx<float> q = mk(1.0f, 0.0f);
+            if (fres) {
+                q = cmul(a.q_row[m], qn);
+                x = cmulc(x, q);
+            }
+            const float amp = a.beam ? __ldg(a.beam + size_t(m) * a.W + n) : 1.0f;
+            const float m2 = x.x * x.x + x.y * x.y;
+            cx<float> h;
+            if (m2 > 0.0f) {
+                const float k = amp * rsqrtf(m2);
+                h = mk(x.x * k, x.y * k);
+            } else {
+                h = mk(amp, 0.0f);
+            }
+            int k;
+            if (a.binary) k = h.x < 0.0f ? 1 : 0;   // PhaseOnly(2, 0): |arg| > pi/2 <=> Re < 0 (up to rounding at Re = 0)
+            else k = quantize_index<float>(a.scheme, h);
+            ip[size_t(m) * a.W] = uint8_t(k);
+            cx<float> sv = state_value<float>(a.scheme, k);
+            if (fres) sv = cmul(sv, q);
+            v[r] = sv;
+        }
+        fast_fft<N, TH, -1>(v, line, t, pt, tw);
+        float2* dst = a.data + size_t(f) * N * a.W + n + size_t(t) * a.W;
+        const size_t step = size_t(TF) * a.W;
+#pragma unroll
+        for (int r = 0; r < 16; ++r) dst[r * step] = make_float2(v[r].x, v[r].y);
+        fence_proxy_async();
+        __syncthreads();
+        if (tid == 0) {
+            const int nt = int(next);
+            tileq[s] = nt;
+            if (nt < ntiles) issue(s, nt);
+        }
+    }
+    pdl_trigger();
+    __syncthreads();
+    finish_ctas(a.tile_ctr);
+}
+
+// ============================================== OSPR replay rows: K1 and K3
+// Jump of k steps of the PCG64 LCG as an affine map s -> A s + inc * G
+// (A = MULT^k, G = sum_{i<k} MULT^i), independent of the stream increment.
+struct LcgJump {
+    u128 A, G;
+};
+__device__ __forceinline__ LcgJump lcg_jump(uint64_t k) {
+    u128 acc_m = 1, acc_g = 0, cur_m = pcg_mult(), cur_g = 1;
+    while (k) {
+        if (k & 1) {
+            acc_g = acc_g * cur_m + cur_g;
+            acc_m *= cur_m;
+        }
+        cur_g = (cur_m + 1) * cur_g;
+        cur_m *= cur_m;
+        k >>= 1;
+    }
+    LcgJump j;
+    j.A = acc_m;
+    j.G = acc_g;
+    return j;
+}
+
+// Start state of every (subframe, centred row) line: stream advanced by uc*W.
+__global__ void ospr_line_states(const Pcg64* __restrict__ frame_rng, int frame0, int frames, int H, int W,
+                                 Pcg64* __restrict__ out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= frames * H) return;
+    const int f = i / H, uc = i - f * H;
+    Pcg64 g = frame_rng[frame0 + f];
+    pcg_advance(g, uint64_t(uc) * uint64_t(W));
+    out[i] = g;
+}
+
+struct FastOsprArgs {
+    float2* data;                 // frames x H x W
+    int H, W, frames;             // frames in this group (local index)
+    int frame0, nframes_total;
+    const float* tgt;             // row-major shifted |T|, sign = outside mask
+    const Pcg64* line_state;      // [frames][H] line start states
+    const cx<float>* tw_row;
+    float scale;
+    float* intensity;             // carried |R|^2 (H*W) or nullptr
+    int load_intensity, store_intensity;
+    double* line_part;            // K3: [frames*3 + 2][H] per-line partial sums
+    unsigned* tile_ctr;
+};
+
+// K1: random-phase sub-target of row u (uncentred) -> inverse row FFT.
+template <int N, int TH, int MINB>
+__global__ void __launch_bounds__(TH, MINB) fast_ospr_gen(FastOsprArgs a) {
+    using S = FastShape<N, TH>;
+    constexpr int TF = S::TF, LW = S::LW;
+    constexpr int SLOT = (LW + 15) / 16 * 16;
+    static_assert(TF % 32 == 0, "row groups must be whole warps");
+    extern __shared__ __align__(128) float2 fsm[];
+    const int tid = threadIdx.x, g = tid / TF, t = tid - g * TF;
+    const int pt = padc(t);
+    const int bid = 1 + g;
+    float2* line = fsm + g * SLOT;
+    __shared__ int lineq[8];
+    FastTw<N, TH> tw;
+    fast_tw_init<N, TH>(tw, t, a.tw_row);
+    const LcgJump jt = lcg_jump(uint64_t(16) * t);   // this thread's chunk offset in the row
+    pdl_wait();
+    const int nlines = a.frames * a.H;
+    for (;;) {
+        if (t == 0) lineq[g] = int(atomicAdd(a.tile_ctr, 1u));
+        group_sync(bid, TF);
+        const int ln = lineq[g];
+        if (ln >= nlines) break;
+        const int f = ln / a.H, u = ln - f * a.H;
+        const int uc = (u + a.H / 2) % a.H;
+        const Pcg64 s0 = a.line_state[f * a.H + uc];
+        Pcg64 gen;
+        gen.state = jt.A * s0.state + s0.inc * jt.G;
+        gen.inc = s0.inc;
+        gen.has_uint32 = 0;
+        gen.uinteger = 0;
+        const float* trow = a.tgt + size_t(u) * N;
+#pragma unroll 4
+        for (int e = 0; e < 16; ++e) {
+            double x = 2.0 * pcg_next_double(gen);   // angle / pi in [0, 2)
+            if (x > 1.0) x -= 2.0;
+            float sn, cs;
+            sincospif(float(x), &sn, &cs);
+            const int pos = (16 * t + e + N / 2) & (N - 1);   // uncentred column of centred 16t+e
+            const float amp = fabsf(trow[pos]);
+            line[padc(pos)] = make_float2(amp * cs, amp * sn);
+        }
+        group_sync(bid, TF);
+        cx<float> v[16];
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+            const float2 z = line[pt + r * TF + (r * TF) / 16];
+            v[r] = mk(z.x, z.y);
+        }
+        fast_fft<N, TH, +1>(v, line, t, pt, tw, bid, TF);
+        float2* dst = a.data + (size_t(f) * a.H + u) * N + t;
+#pragma unroll
+        for (int r = 0; r < 16; ++r) dst[r * TF] = make_float2(v[r].x, v[r].y);
+        group_sync(bid, TF);
+    }
+    pdl_trigger();
+    __syncthreads();
+    finish_ctas(a.tile_ctr);
+}
+
+// K3: row u of every subframe in the group: forward row FFT, running
+// intensity sum, per-frame masked error partials of sqrt(I / i) -> per-line
+// slots (fixed-order totals in ospr_line_reduce). Twiddles from a shared table.
+template <int N, int TH, int MINB>
+__global__ void __launch_bounds__(TH, MINB) fast_ospr_acc(FastOsprArgs a) {
+    using S = FastShape<N, TH>;
+    constexpr int TF = S::TF, LW = S::LW, GROUPS = S::LINES;
+    constexpr int SLOT = (LW + 15) / 16 * 16;
+    constexpr uint32_t LINE_BYTES = uint32_t(N) * 8u;
+    constexpr int WPG = TF / 32;   // warps per group
+    static_assert(TF % 32 == 0, "row groups must be whole warps");
+    extern __shared__ __align__(128) float2 fsm[];
+    __shared__ __align__(8) uint64_t full[GROUPS][2];
+    __shared__ int lineq[GROUPS];
+    __shared__ double wsum[GROUPS][WPG][3];
+    const int tid = threadIdx.x, g = tid / TF, t = tid - g * TF;
+    const int lane = t & 31, wg = t >> 5;
+    const int pt = padc(t);
+    const int bid = 1 + g;
+    float2* tab = fsm;
+    float2* slots = fsm + TwTables<N, TH>::WORDS + g * 2 * SLOT;
+    TwTables<N, TH>::load(tab, a.tw_row);
+    if (t == 0) {
+        mbar_init(&full[g][0], 1);
+        mbar_init(&full[g][1], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    pdl_wait();
+    const size_t fstride = size_t(a.H) * N;
+    int uses[2] = {0, 0};
+    for (;;) {
+        if (t == 0) lineq[g] = int(atomicAdd(a.tile_ctr, 1u));
+        group_sync(bid, TF);
+        const int u = lineq[g];
+        if (u >= a.H) break;
+        const float* trow = a.tgt + size_t(u) * N + t;
+        float tv[16], inten[16];
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+            tv[r] = trow[r * TF];
+            inten[r] = a.load_intensity ? a.intensity[size_t(u) * N + t + r * TF] : 0.0f;
+        }
+        if (t == 0) {
+#pragma unroll
+            for (int s = 0; s < 2; ++s)
+                if (s < a.frames) {
+                    mbar_expect_tx(&full[g][s], LINE_BYTES);
+                    bulk_g2s(slots + s * SLOT, a.data + size_t(s) * fstride + size_t(u) * N, LINE_BYTES, &full[g][s]);
+                }
+        }
+        for (int f = 0; f < a.frames; ++f) {
+            const int s = f & 1;
+            float2* line = slots + s * SLOT;
+            mbar_wait(&full[g][s], uses[s] & 1);
+            uses[s] += 1;
+            cx<float> v[16];
+#pragma unroll
+            for (int r = 0; r < 16; ++r) {
+                const float2 z = line[t + r * TF];
+                v[r] = mk(z.x, z.y);
+            }
+            fast_fft_s<N, TH, -1>(v, line, t, pt, tab, bid, TF);
+            const float inv_n = 1.0f / float(a.frame0 + f + 1);
+            float sdd = 0.f, spp = 0.f, spd = 0.f;
+#pragma unroll
+            for (int r = 0; r < 16; ++r) {
+                const float x = v[r].x * a.scale, y = v[r].y * a.scale;
+                inten[r] += x * x + y * y;
+                const bool in = !signbit(tv[r]);
+                const float p = sqrtf(inten[r] * inv_n);
+                const float d = p - tv[r];
+                sdd += in ? d * d : 0.f;
+                spp += in ? p * p : 0.f;
+                spd += in ? p * d : 0.f;
+            }
+            double w3[3] = {double(sdd), double(spp), double(spd)};
+#pragma unroll
+            for (int q = 0; q < 3; ++q)
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) w3[q] += __shfl_xor_sync(0xffffffffu, w3[q], o);
+            if (lane == 0) {
+                wsum[g][wg][0] = w3[0];
+                wsum[g][wg][1] = w3[1];
+                wsum[g][wg][2] = w3[2];
+            }
+            fence_proxy_async();
+            group_sync(bid, TF);
+            if (t == 0) {
+#pragma unroll
+                for (int q = 0; q < 3; ++q) {
+                    double acc = 0;
+                    for (int w = 0; w < WPG; ++w) acc += wsum[g][w][q];
+                    a.line_part[(size_t(3 * f + q)) * a.H + u] = acc;
+                }
+                if (f + 2 < a.frames) {
+                    mbar_expect_tx(&full[g][s], LINE_BYTES);
+                    bulk_g2s(line, a.data + size_t(f + 2) * fstride + size_t(u) * N, LINE_BYTES, &full[g][s]);
+                }
+            }
+            group_sync(bid, TF);
+        }
+        if (a.frame0 + a.frames == a.nframes_total) {
+            const float inv_n = 1.0f / float(a.nframes_total);
+            float sin_ = 0.f, sall = 0.f;
+#pragma unroll
+            for (int r = 0; r < 16; ++r) {
+                const float p = sqrtf(inten[r] * inv_n);
+                const float pp = p * p;
+                sall += pp;
+                sin_ += !signbit(tv[r]) ? pp : 0.f;
+            }
+            double w2[2] = {double(sin_), double(sall)};
+#pragma unroll
+            for (int q = 0; q < 2; ++q)
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) w2[q] += __shfl_xor_sync(0xffffffffu, w2[q], o);
+            if (lane == 0) {
+                wsum[g][wg][0] = w2[0];
+                wsum[g][wg][1] = w2[1];
+            }
+            group_sync(bid, TF);
+            if (t == 0) {
+                for (int q = 0; q < 2; ++q) {
+                    double acc = 0;
+                    for (int w = 0; w < WPG; ++w) acc += wsum[g][w][q];
+                    a.line_part[(size_t(3 * a.frames + q)) * a.H + u] = acc;
+                }
+            }
+        }
+        if (a.store_intensity) {
+#pragma unroll
+            for (int r = 0; r < 16; ++r) a.intensity[size_t(u) * N + t + r * TF] = inten[r];
+        }
+        group_sync(bid, TF);
+    }
+    pdl_trigger();
+    __syncthreads();
+    finish_ctas(a.tile_ctr);
+}
+
+// Fixed-order totals of the per-line partials: one CTA per quantity.
+__global__ void ospr_line_reduce(const double* __restrict__ line_part, int H, int frames, int frame0, int tail,
+                                 int nframes_total, const double* __restrict__ denom, int rescale,
+                                 double* __restrict__ out) {
+    // block f < frames: frame error; block == frames: efficiency (tail only)
+    const int f = blockIdx.x;
+    __shared__ double sh[32 * 3];
+    const int nq = (f < frames) ? 3 : 2;
+    double acc[3] = {0, 0, 0};
+    for (int u = threadIdx.x; u < H; u += blockDim.x)
+        for (int q = 0; q < nq; ++q) acc[q] += line_part[size_t(3 * f + q) * H + u];
+    block_reduce<3>(acc, sh);
+    if (threadIdx.x == 0) {
+        if (f < frames) out[frame0 + f] = error_from_sums(acc[0], acc[1], acc[2], *denom, rescale);
+        else if (tail) out[nframes_total] = acc[1] == 0.0 ? __longlong_as_double(0x7ff8000000000000LL) : acc[0] / acc[1];
     }
 }
 

@@ -547,15 +547,34 @@ static int ospr_exec(cgh_plan* P, const cgh_ospr_params* op, int64_t* tk, double
         PassArgs<T> b = a;
         b.frame0 = g0;
         b.frames = m;
-        CGH_TRY(run_row<T>(P, ROW_OSPR_GEN, b, m));
+        bool fast_ospr = false;
+        if constexpr (sizeof(T) == 4) fast_ospr = fast_ospr_eligible(P);
+        if constexpr (sizeof(T) == 4) {
+            if (fast_ospr) CGH_TRY(fast_ospr_gen(P, b));
+            else CGH_TRY(run_row<T>(P, ROW_OSPR_GEN, b, m));
+        } else {
+            CGH_TRY(run_row<T>(P, ROW_OSPR_GEN, b, m));
+        }
         b.quantize = 1;
         b.idx_out = static_cast<uint8_t*>(P->idx.p) + size_t(g0) * n * P->idx_bytes;
-        CGH_TRY(run_col<T>(P, COL_HOLO, b, m));
+        bool fast_done = false;
+        if constexpr (sizeof(T) == 4) {
+            if (fast_ospr_eligible(P)) {
+                CGH_TRY(fast_ospr_holo(P, b, m, std::max(G, 1), static_cast<uint8_t*>(b.idx_out)));
+                fast_done = true;
+            }
+        }
+        if (!fast_done) CGH_TRY(run_col<T>(P, COL_HOLO, b, m));
         b.idx_out = nullptr;
         b.quantize = 0;
         b.load_intensity = g0 > 0 ? 1 : 0;
         b.store_intensity = (carry || has_cancel) ? 1 : 0;
-        CGH_TRY(run_row<T>(P, ROW_OSPR_ACC, b, 1));
+        if constexpr (sizeof(T) == 4) {
+            if (fast_ospr) CGH_TRY(fast_ospr_acc(P, b));
+            else CGH_TRY(run_row<T>(P, ROW_OSPR_ACC, b, 1));
+        } else {
+            CGH_TRY(run_row<T>(P, ROW_OSPR_ACC, b, 1));
+        }
         done = g0 + m;
         if (has_progress || has_cancel) {
             for (int f = g0; f < g0 + m; ++f) CGH_TRY(pq.push(f));

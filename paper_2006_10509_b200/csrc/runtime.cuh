@@ -103,6 +103,10 @@ int fast_row(cgh_plan* P, const PassArgs<float>& a);
 int fast_col(cgh_plan* P, const PassArgs<float>& a);
 void fast_free(cgh_plan* P);
 void fast_invalidate_target(cgh_plan* P);
+bool fast_ospr_eligible(cgh_plan* P);
+int fast_ospr_holo(cgh_plan* P, const PassArgs<float>& a, int frames, int cap, uint8_t* idx_out);
+int fast_ospr_gen(cgh_plan* P, const PassArgs<float>& a);
+int fast_ospr_acc(cgh_plan* P, const PassArgs<float>& a);
 
 // Record a timing event before (start) / after a pass launch. Pass ids:
 // row modes 0..7, column modes 8 + mode, search kernels 16+.

@@ -108,3 +108,60 @@ def test_c3_per_iteration_field_fp32():
         _, fld, _, _ = _field(cfg, target, fast=True)
         err = np.linalg.norm(fld - ref.fields[k]) / np.linalg.norm(ref.fields[k])
         assert err < 1e-4, (k, err)
+
+
+def _ospr(cfg, target, illum=None, fast=True, progress=None):
+    old = os.environ.pop("CGHB200_NO_FAST", None)
+    if not fast:
+        os.environ["CGHB200_NO_FAST"] = "1"
+    try:
+        with precision("fp32"):
+            return A.run_ospr(cfg, target, illum, progress=progress)
+    finally:
+        os.environ.pop("CGHB200_NO_FAST", None)
+        if old is not None:
+            os.environ["CGHB200_NO_FAST"] = old
+
+
+@pytest.mark.parametrize("h,w,kind,levels,beam,mask,frames", [
+    (1024, 1024, "fourier", 2, False, False, 6),
+    (512, 1024, "fresnel", 4, True, True, 3),
+    (2048, 512, "fourier", 8, False, True, 2),
+])
+def test_fast_ospr_matches_generic(h, w, kind, levels, beam, mask, frames):
+    from paper_2006_10509_b200.slm import PhaseOnly as PO
+
+    rects = [(w // 8, h // 8, w // 2, h // 3)] if mask else []
+    cfg = A.AlgorithmConfig("ospr", SlmSpec(w, h, PO(levels)), PropagationSpec(kind),
+                            MetricSpec(rect_mask(w, h, rects), rescale=mask), seed=9, subframes=frames)
+    target = natural_target(w, h) if h != w else natural_target(w)
+    illum = gaussian_beam(h, w) if beam else None
+    f1, r1 = _ospr(cfg, target, illum, fast=True)
+    f2, r2 = _ospr(cfg, target, illum, fast=False)
+    assert len(f1) == len(f2) == frames
+    mism = sum(int(np.sum(a != b)) for a, b in zip(f1, f2))
+    assert mism <= max(4, h * w * frames // 20000), mism
+    e1 = np.array([e for _, e in r1.error_trace])
+    e2 = np.array([e for _, e in r2.error_trace])
+    assert np.max(np.abs(e1 - e2) / e2) < 1e-4
+    assert abs(r1.efficiency - r2.efficiency) < 1e-5
+    # progress path: one subframe per launch group, carried intensity
+    seen = []
+    f3, r3 = _ospr(cfg, target, illum, fast=True, progress=lambda k, e: seen.append(k))
+    assert seen == list(range(1, frames + 1))
+    assert all(np.array_equal(a, b) for a, b in zip(f1, f3))
+    assert np.max(np.abs(np.array([e for _, e in r3.error_trace]) - e1) / e1) < 1e-6
+
+
+def test_c2_full_size_fp32_fast():
+    name = "C2_ospr_1024_bin_24"
+    rec = MAN[name]
+    cfg, target, illum = G.build(rec)
+    arrs = G.load_arrays(name)
+    table = states(cfg.slm.scheme)
+    frames, rep = _ospr(cfg, target, illum, fast=True)
+    tr = np.array([e for _, e in rep.error_trace])
+    assert np.max(np.abs(tr - arrs["trace"]) / arrs["trace"]) < 1e-3
+    assert abs(rep.efficiency - rec["efficiency"]) < 1e-4
+    for i in (0, len(frames) - 1):
+        assert np.sum(frames[i] != table[arrs[f"idx{i}"]]) <= 64
