@@ -188,7 +188,7 @@ static cudaError_t row_launch(cgh_plan* P, const FastArgs& f) {
     if (row_variant() == 3) return row_launch_s<N, 3>(P, f);
     if (row_variant() == 4) return row_launch_s<N, 4>(P, f);
     using S = FastShape<N, kRowTH>;
-    const size_t smem = size_t(2) * S::LINES * ((S::LW + 15) / 16 * 16) * sizeof(float2);
+    const size_t smem = size_t(3) * S::LINES * ((S::LW + 15) / 16 * 16) * sizeof(float2);
     auto k = fast_row_holo<N, kRowTH, kRowMinB>;
     static bool attr = false;
     if (!attr) {

@@ -38,35 +38,57 @@ struct FastShape {
     static constexpr int R2 = N / NS2;                     // stage-3 radix (1 = none)
 };
 
+// Per-thread Stockham twiddles in compact form: for each butterfly only the
+// powers w, w^2, w^4, w^8 of its base root (exp(-2 pi i (j mod NS)/(NS R)))
+// are kept in registers; w^r is formed from them with at most 3 complex
+// products (<= ~4 ulp). Keeping all 29 twiddles made ptxas rematerialise them
+// as global loads inside the butterflies (ncu: long-scoreboard stalls).
 template <int N, int TH>
 struct FastTw {
-    cx<float> w1[16];   // stage 2 (NS = 16)
-    cx<float> w2[16];   // stage 3 (NS = 16*R1)
+    cx<float> p1[4];        // stage 2 (NS = 16): powers 1, 2, 4, 8
+    cx<float> p2[16 / 2][3];   // stage 3: per butterfly b, powers 1, 2, 4 (R2 <= 8) or see p2x
+    cx<float> p2x[4];       // stage 3 with R2 == 16 (N = 4096): powers 1, 2, 4, 8 (NB = 1)
 };
 
 template <int N, int TH>
 __device__ __forceinline__ void fast_tw_init(FastTw<N, TH>& tw, int t, const cx<float>* __restrict__ table) {
     using S = FastShape<N, TH>;
     {
-        constexpr int NS = 16, R = S::R1, NB = 16 / R;
+        constexpr int NS = 16, R = S::R1;
+        const int jm = t & (NS - 1);
 #pragma unroll
-        for (int b = 0; b < NB; ++b)
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-                const int j = t + b * S::TF;
-                tw.w1[b * R + r] = ldg_cx(table + (j & (NS - 1)) * r * (N / (NS * R)));
-            }
+        for (int k = 0; k < 4; ++k) tw.p1[k] = ldg_cx(table + ((jm << k) * (N / (NS * R))) % N);
     }
     if constexpr (S::R2 > 1) {
         constexpr int NS = S::NS2, R = S::R2, NB = 16 / R;
+        if constexpr (R == 16) {
+            const int jm = t & (NS - 1);
 #pragma unroll
-        for (int b = 0; b < NB; ++b)
+            for (int k = 0; k < 4; ++k) tw.p2x[k] = ldg_cx(table + ((jm << k) * (N / (NS * R))) % N);
+        } else {
 #pragma unroll
-            for (int r = 0; r < R; ++r) {
-                const int j = t + b * S::TF;
-                tw.w2[b * R + r] = ldg_cx(table + (j & (NS - 1)) * r * (N / (NS * R)));
+            for (int b = 0; b < NB; ++b) {
+                const int jm = (t + b * S::TF) & (NS - 1);
+#pragma unroll
+                for (int k = 0; k < 3; ++k) tw.p2[b][k] = ldg_cx(table + ((jm << k) * (N / (NS * R))) % N);
             }
+        }
     }
+}
+
+// w^r from the stored powers (r compile-time, 1 <= r < 16)
+template <int R>
+__device__ __forceinline__ cx<float> pow_from(const cx<float>* p) {
+    cx<float> w = mk(1.0f, 0.0f);
+    bool first = true;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        if ((R >> k) & 1) {
+            w = first ? p[k] : cmul(w, p[k]);
+            first = false;
+        }
+    }
+    return w;
 }
 
 // compile-time offset K added to a padded index whose base is 16-aligned in
@@ -83,34 +105,51 @@ __device__ __forceinline__ void group_sync(int id, int count) {
 
 // Twiddle sources: per-thread registers (RegTw) or a shared-memory table
 // laid out [r][j mod NS] (SmemTw; lanes read consecutive entries).
-struct RegTw {
-    const cx<float>* w;
-    template <int NS, int R, int TF>
-    __device__ __forceinline__ cx<float> get(int, int b, int r) const { return w[b * R + r]; }
+// compact register powers: stage with NB butterflies per thread, powers per b
+struct PowTw {
+    const cx<float>* p;   // p[b * stride + k]
+    int stride;
 };
-struct SmemTw {
-    const float2* tab;   // this stage's table
-    template <int NS, int R, int TF>
-    __device__ __forceinline__ cx<float> get(int t, int b, int r) const {
-        const float2 z = tab[r * NS + ((t + b * TF) & (NS - 1))];
-        return mk(z.x, z.y);
-    }
-};
+struct RegTw {};
 
-template <int N, int TH, int DIR, int NS, int R, bool LAST, class TW>
+template <int DIR, int R, int NB, int RR>
+__device__ __forceinline__ void apply_pow(cx<float> (&v)[16], const cx<float>* p, int b) {
+    if constexpr (RR < R) {
+        const cx<float> w = pow_from<RR>(p);
+        v[b * R + RR] = DIR < 0 ? cmul(v[b * R + RR], w) : cmulc(v[b * R + RR], w);
+        apply_pow<DIR, R, NB, RR + 1>(v, p, b);
+    }
+}
+
+template <int DIR, int R, int NB>
+__device__ __forceinline__ void apply_tw(cx<float> (&v)[16], const PowTw& tw, int) {
+#pragma unroll
+    for (int b = 0; b < NB; ++b) apply_pow<DIR, R, NB, 1>(v, tw.p + b * tw.stride, b);
+}
+template <int DIR, int R, int NB>
+__device__ __forceinline__ void apply_tw(cx<float> (&v)[16], const RegTw&, int) {}
+template <int NS_, int TF_>
+struct SmemTw {
+    const float2* tab;   // this stage's table [r][j mod NS]
+};
+template <int DIR, int R, int NB, int NS_, int TF_>
+__device__ __forceinline__ void apply_tw(cx<float> (&v)[16], const SmemTw<NS_, TF_>& tw, int t) {
+#pragma unroll
+    for (int b = 0; b < NB; ++b)
+#pragma unroll
+        for (int r = 1; r < R; ++r) {
+            const float2 z = tw.tab[r * NS_ + ((t + b * TF_) & (NS_ - 1))];
+            const cx<float> w = mk(z.x, z.y);
+            v[b * R + r] = DIR < 0 ? cmul(v[b * R + r], w) : cmulc(v[b * R + r], w);
+        }
+}
+
+template <int N, int TH, int DIR, int NS, int R, bool LAST, class TW, bool PRE = true>
 __device__ __forceinline__ void fast_stage(cx<float> (&v)[16], float2* sm, int t, int pt, const TW& tw, int bid,
                                            int bcount) {
     using S = FastShape<N, TH>;
     constexpr int NB = 16 / R;
-    if constexpr (NS > 1) {
-#pragma unroll
-        for (int b = 0; b < NB; ++b)
-#pragma unroll
-            for (int r = 1; r < R; ++r) {
-                const cx<float> w = tw.template get<NS, R, S::TF>(t, b, r);
-                v[b * R + r] = DIR < 0 ? cmul(v[b * R + r], w) : cmulc(v[b * R + r], w);
-            }
-    }
+    if constexpr (NS > 1) apply_tw<DIR, R, NB>(v, tw, t);
 #pragma unroll
     for (int b = 0; b < NB; ++b) Dft<R, DIR, 1, float>::run(&v[b * R]);
     if constexpr (LAST) {
@@ -124,7 +163,7 @@ __device__ __forceinline__ void fast_stage(cx<float> (&v)[16], float2* sm, int t
                 for (int r = 0; r < R; ++r) v[b + r * NB] = tmp[b * R + r];
         }
     } else if (bid >= 0) {   // bid < 0: exchange skipped (timing experiments only)
-        group_sync(bid, bcount);
+        if constexpr (PRE) group_sync(bid, bcount);   // PRE = false: caller alternates buffers
 #pragma unroll
         for (int b = 0; b < NB; ++b) {
             const int j = t + b * S::TF;
@@ -150,12 +189,40 @@ template <int N, int TH, int DIR>
 __device__ __forceinline__ void fast_fft(cx<float> (&v)[16], float2* sm, int t, int pt, const FastTw<N, TH>& tw,
                                          int bid = 0, int bcount = TH) {
     using S = FastShape<N, TH>;
-    fast_stage<N, TH, DIR, 1, 16, false>(v, sm, t, pt, RegTw{nullptr}, bid, bcount);
+    fast_stage<N, TH, DIR, 1, 16, false>(v, sm, t, pt, RegTw{}, bid, bcount);
     if constexpr (S::R2 > 1) {
-        fast_stage<N, TH, DIR, 16, S::R1, false>(v, sm, t, pt, RegTw{tw.w1}, bid, bcount);
-        fast_stage<N, TH, DIR, S::NS2, S::R2, true>(v, sm, t, pt, RegTw{tw.w2}, bid, bcount);
+        fast_stage<N, TH, DIR, 16, S::R1, false>(v, sm, t, pt, PowTw{tw.p1, 0}, bid, bcount);
+        if constexpr (S::R2 == 16)
+            fast_stage<N, TH, DIR, S::NS2, S::R2, true>(v, sm, t, pt, PowTw{tw.p2x, 0}, bid, bcount);
+        else
+            fast_stage<N, TH, DIR, S::NS2, S::R2, true>(v, sm, t, pt, PowTw{&tw.p2[0][0], 3}, bid, bcount);
     } else {
-        fast_stage<N, TH, DIR, 16, S::R1, true>(v, sm, t, pt, RegTw{tw.w1}, bid, bcount);
+        fast_stage<N, TH, DIR, 16, S::R1, true>(v, sm, t, pt, PowTw{tw.p1, 0}, bid, bcount);
+    }
+}
+
+// Number of shared-memory exchanges in one transform (2 for N > 256).
+template <int N, int TH>
+constexpr int fast_exchanges() { return FastShape<N, TH>::R2 > 1 ? 2 : 1; }
+
+// Ping-pong variant: exchange e goes to buffer e & 1 with a single barrier
+// (after the writes). A write into a buffer is safe once a barrier has passed
+// after that buffer's last read, which holds when the caller keeps the
+// buffers alternating across consecutive transforms.
+template <int N, int TH, int DIR>
+__device__ __forceinline__ void fast_fft_pp(cx<float> (&v)[16], float2* b0, float2* b1, int t, int pt,
+                                            const FastTw<N, TH>& tw, int bid, int bcount) {
+    using S = FastShape<N, TH>;
+    if constexpr (S::R2 > 1) {
+        fast_stage<N, TH, DIR, 1, 16, false, RegTw, false>(v, b0, t, pt, RegTw{}, bid, bcount);
+        fast_stage<N, TH, DIR, 16, S::R1, false, PowTw, false>(v, b1, t, pt, PowTw{tw.p1, 0}, bid, bcount);
+        if constexpr (S::R2 == 16)
+            fast_stage<N, TH, DIR, S::NS2, S::R2, true>(v, b1, t, pt, PowTw{tw.p2x, 0}, bid, bcount);
+        else
+            fast_stage<N, TH, DIR, S::NS2, S::R2, true>(v, b1, t, pt, PowTw{&tw.p2[0][0], 3}, bid, bcount);
+    } else {
+        fast_stage<N, TH, DIR, 1, 16, false, RegTw, false>(v, b0, t, pt, RegTw{}, bid, bcount);
+        fast_stage<N, TH, DIR, 16, S::R1, true>(v, b0, t, pt, PowTw{tw.p1, 0}, bid, bcount);
     }
 }
 
@@ -184,12 +251,13 @@ template <int N, int TH, int DIR>
 __device__ __forceinline__ void fast_fft_s(cx<float> (&v)[16], float2* sm, int t, int pt, const float2* tab, int bid,
                                            int bcount) {
     using S = FastShape<N, TH>;
-    fast_stage<N, TH, DIR, 1, 16, false>(v, sm, t, pt, RegTw{nullptr}, bid, bcount);
+    fast_stage<N, TH, DIR, 1, 16, false>(v, sm, t, pt, RegTw{}, bid, bcount);
     if constexpr (S::R2 > 1) {
-        fast_stage<N, TH, DIR, 16, S::R1, false>(v, sm, t, pt, SmemTw{tab}, bid, bcount);
-        fast_stage<N, TH, DIR, S::NS2, S::R2, true>(v, sm, t, pt, SmemTw{tab + TwTables<N, TH>::T2}, bid, bcount);
+        fast_stage<N, TH, DIR, 16, S::R1, false>(v, sm, t, pt, SmemTw<16, S::TF>{tab}, bid, bcount);
+        fast_stage<N, TH, DIR, S::NS2, S::R2, true>(v, sm, t, pt, SmemTw<S::NS2, S::TF>{tab + TwTables<N, TH>::T2},
+                                                   bid, bcount);
     } else {
-        fast_stage<N, TH, DIR, 16, S::R1, true>(v, sm, t, pt, SmemTw{tab}, bid, bcount);
+        fast_stage<N, TH, DIR, 16, S::R1, true>(v, sm, t, pt, SmemTw<16, S::TF>{tab}, bid, bcount);
     }
 }
 
@@ -244,6 +312,7 @@ __global__ void __launch_bounds__(TH, MINB) fast_row_holo(FastArgs a) {
     constexpr int TF = S::TF, GROUPS = S::LINES, LW = S::LW;
     constexpr int SLOT = (LW + 15) / 16 * 16;   // one padded line, 128-B aligned
     constexpr uint32_t LINE_BYTES = uint32_t(N) * 8u;
+    constexpr bool TWO = fast_exchanges<N, TH>() == 2;
     static_assert(TF % 32 == 0, "row groups must be whole warps");
     extern __shared__ __align__(128) float2 fsm[];
     __shared__ __align__(8) uint64_t full[GROUPS][2];
@@ -253,7 +322,8 @@ __global__ void __launch_bounds__(TH, MINB) fast_row_holo(FastArgs a) {
     const int pt = padc(t);
     const int nlines = a.H;
     const int bid = 1 + g;
-    float2* slots = fsm + g * 2 * SLOT;
+    float2* slots = fsm + g * 3 * SLOT;   // [slot 0][slot 1][exchange X]
+    float2* xb = slots + 2 * SLOT;
     FastTw<N, TH> tw;
     fast_tw_init<N, TH>(tw, t, a.tw_row);
     if (lead) {
@@ -262,28 +332,29 @@ __global__ void __launch_bounds__(TH, MINB) fast_row_holo(FastArgs a) {
         mbar_fence_init();
     }
     pdl_wait();
+    auto issue = [&](int s, int m) {
+        if (a.debug & 2) {
+            mbar_expect_tx(&full[g][s], 0);
+        } else {
+            mbar_expect_tx(&full[g][s], LINE_BYTES);
+            bulk_g2s(slots + s * SLOT, a.data + size_t(m) * N, LINE_BYTES, &full[g][s]);
+        }
+    };
     if (lead) {
 #pragma unroll
         for (int s = 0; s < 2; ++s) {
             const int m = int(atomicAdd(a.tile_ctr, 1u));
             lineq[g][s] = m;
-            if (m < nlines) {
-                if (a.debug & 2) {
-                    mbar_expect_tx(&full[g][s], 0);
-                } else {
-                    mbar_expect_tx(&full[g][s], LINE_BYTES);
-                    bulk_g2s(slots + s * SLOT, a.data + size_t(m) * N, LINE_BYTES, &full[g][s]);
-                }
-            }
+            if (m < nlines) issue(s, m);
         }
     }
     group_sync(bid, TF);
+    unsigned next = 0;
+    if (lead) next = atomicAdd(a.tile_ctr, 1u);   // refill of slot 1 after line 0
     for (int it = 0;; ++it) {
         const int s = it & 1;
         const int m = lineq[g][s];
         if (m >= nlines) break;
-        unsigned next = 0;
-        if (lead) next = atomicAdd(a.tile_ctr, 1u);
         float2* line = slots + s * SLOT;
         mbar_wait(&full[g][s], (it >> 1) & 1);
         cx<float> v[16];
@@ -292,7 +363,25 @@ __global__ void __launch_bounds__(TH, MINB) fast_row_holo(FastArgs a) {
             const float2 z = line[t + r * TF];
             v[r] = mk(z.x, z.y);
         }
-        if (a.debug != 1) fast_fft<N, TH, +1>(v, line, t, pt, tw, (a.debug & 4) ? -1 : bid, TF);
+        // Exchange buffers alternate X, line, X, line (X, line for one-exchange
+        // sizes). The first exchange barrier also retires every read of the
+        // other slot (previous line), so its refill is issued right after it.
+        fast_stage<N, TH, +1, 1, 16, false, RegTw, false>(v, xb, t, pt, RegTw{}, bid, TF);
+        if (it > 0 && lead) {
+            const int nm = int(next);
+            lineq[g][s ^ 1] = nm;
+            if (nm < nlines) issue(s ^ 1, nm);
+            next = atomicAdd(a.tile_ctr, 1u);
+        }
+        if constexpr (TWO) {
+            fast_stage<N, TH, +1, 16, S::R1, false, PowTw, false>(v, line, t, pt, PowTw{tw.p1, 0}, bid, TF);
+            if constexpr (S::R2 == 16)
+                fast_stage<N, TH, +1, S::NS2, S::R2, true>(v, line, t, pt, PowTw{tw.p2x, 0}, bid, TF);
+            else
+                fast_stage<N, TH, +1, S::NS2, S::R2, true>(v, line, t, pt, PowTw{&tw.p2[0][0], 3}, bid, TF);
+        } else {
+            fast_stage<N, TH, +1, 16, S::R1, true>(v, xb, t, pt, PowTw{tw.p1, 0}, bid, TF);
+        }
 #pragma unroll
         for (int r = 0; r < 16; ++r) {
             const float amp = a.beam ? __ldg(a.beam + size_t(m) * N + t + r * TF) : 1.0f;
@@ -306,27 +395,14 @@ __global__ void __launch_bounds__(TH, MINB) fast_row_holo(FastArgs a) {
                 v[r] = h;
             }
         }
-        if (a.debug != 1) fast_fft<N, TH, -1>(v, line, t, pt, tw, (a.debug & 4) ? -1 : bid, TF);
+        if constexpr (TWO) fast_fft_pp<N, TH, -1>(v, xb, line, t, pt, tw, bid, TF);
+        else fast_fft_pp<N, TH, -1>(v, line, xb, t, pt, tw, bid, TF);
         float2* dst = a.data + size_t(m) * N + t;
         if (!(a.debug & 2)) {
 #pragma unroll
             for (int r = 0; r < 16; ++r) dst[r * TF] = make_float2(v[r].x, v[r].y);
         }
-        fence_proxy_async();
-        group_sync(bid, TF);
-        if (lead) {
-            const int nm = int(next);
-            lineq[g][s] = nm;
-            if (nm < nlines) {
-                if (a.debug & 2) {
-                    mbar_expect_tx(&full[g][s], 0);
-                } else {
-                    mbar_expect_tx(&full[g][s], LINE_BYTES);
-                    bulk_g2s(line, a.data + size_t(nm) * N, LINE_BYTES, &full[g][s]);
-                }
-            }
-        }
-        group_sync(bid, TF);
+        fence_proxy_async();   // generic accesses to this slot before its async refill
     }
     pdl_trigger();
     __syncthreads();
