@@ -30,9 +30,10 @@ struct FastShape {
     static constexpr int E = 16;
     static constexpr int TF = N / E;
     static constexpr int LINES = TH / TF;                  // lines per tile
-    // padded line (float2): 1 word per 16, plus 4 so that lines c = 0..3 of a
-    // column tile start in different banks (LW = 4 mod 16)
-    static constexpr int LW = N + N / 16 + 4;
+    // padded line (float2): 1 word per 16, plus a stagger so that the lines
+    // of a column tile interleaved in one warp start in disjoint bank ranges
+    // (4 lines: LW = 4 mod 16; 2 lines: LW = 8 mod 16)
+    static constexpr int LW = N + N / 16 + (LINES == 2 ? 8 : 4);
     static constexpr int R1 = (N / 16 >= 16) ? 16 : N / 16;   // stage-2 radix
     static constexpr int NS2 = 16 * R1;
     static constexpr int R2 = N / NS2;                     // stage-3 radix (1 = none)
@@ -322,6 +323,7 @@ __global__ void __launch_bounds__(TH, MINB) fast_row_holo(FastArgs a) {
     const int pt = padc(t);
     const int nlines = a.H;
     const int bid = 1 + g;
+    const int fb = bid;
     float2* slots = fsm + g * 3 * SLOT;   // [slot 0][slot 1][exchange X]
     float2* xb = slots + 2 * SLOT;
     FastTw<N, TH> tw;
@@ -366,7 +368,7 @@ __global__ void __launch_bounds__(TH, MINB) fast_row_holo(FastArgs a) {
         // Exchange buffers alternate X, line, X, line (X, line for one-exchange
         // sizes). The first exchange barrier also retires every read of the
         // other slot (previous line), so its refill is issued right after it.
-        fast_stage<N, TH, +1, 1, 16, false, RegTw, false>(v, xb, t, pt, RegTw{}, bid, TF);
+        fast_stage<N, TH, +1, 1, 16, false, RegTw, false>(v, xb, t, pt, RegTw{}, fb, TF);
         if (it > 0 && lead) {
             const int nm = int(next);
             lineq[g][s ^ 1] = nm;
@@ -374,13 +376,13 @@ __global__ void __launch_bounds__(TH, MINB) fast_row_holo(FastArgs a) {
             next = atomicAdd(a.tile_ctr, 1u);
         }
         if constexpr (TWO) {
-            fast_stage<N, TH, +1, 16, S::R1, false, PowTw, false>(v, line, t, pt, PowTw{tw.p1, 0}, bid, TF);
+            fast_stage<N, TH, +1, 16, S::R1, false, PowTw, false>(v, line, t, pt, PowTw{tw.p1, 0}, fb, TF);
             if constexpr (S::R2 == 16)
-                fast_stage<N, TH, +1, S::NS2, S::R2, true>(v, line, t, pt, PowTw{tw.p2x, 0}, bid, TF);
+                fast_stage<N, TH, +1, S::NS2, S::R2, true>(v, line, t, pt, PowTw{tw.p2x, 0}, fb, TF);
             else
-                fast_stage<N, TH, +1, S::NS2, S::R2, true>(v, line, t, pt, PowTw{&tw.p2[0][0], 3}, bid, TF);
+                fast_stage<N, TH, +1, S::NS2, S::R2, true>(v, line, t, pt, PowTw{&tw.p2[0][0], 3}, fb, TF);
         } else {
-            fast_stage<N, TH, +1, 16, S::R1, true>(v, xb, t, pt, PowTw{tw.p1, 0}, bid, TF);
+            fast_stage<N, TH, +1, 16, S::R1, true>(v, xb, t, pt, PowTw{tw.p1, 0}, fb, TF);
         }
 #pragma unroll
         for (int r = 0; r < 16; ++r) {
@@ -395,8 +397,8 @@ __global__ void __launch_bounds__(TH, MINB) fast_row_holo(FastArgs a) {
                 v[r] = h;
             }
         }
-        if constexpr (TWO) fast_fft_pp<N, TH, -1>(v, xb, line, t, pt, tw, bid, TF);
-        else fast_fft_pp<N, TH, -1>(v, line, xb, t, pt, tw, bid, TF);
+        if constexpr (TWO) fast_fft_pp<N, TH, -1>(v, xb, line, t, pt, tw, fb, TF);
+        else fast_fft_pp<N, TH, -1>(v, line, xb, t, pt, tw, fb, TF);
         float2* dst = a.data + size_t(m) * N + t;
         if (!(a.debug & 2)) {
 #pragma unroll
@@ -512,6 +514,10 @@ __global__ void __launch_bounds__(TH, MINB) fast_col_gs(FastArgs a, const __grid
     FastTw<N, TH> tw;
     fast_tw_init<N, TH>(tw, t, a.tw_col);
     auto issue = [&](int s, int tile) {
+        if (a.debug & 2) {   // timing experiment: no tile traffic
+            mbar_expect_tx(&full[s], 0);
+            return;
+        }
         mbar_expect_tx(&full[s], TILE_BYTES + TGT_BYTES);
 #pragma unroll 1
         for (int y = 0; y < N; y += kFastBoxRows)
@@ -552,7 +558,7 @@ __global__ void __launch_bounds__(TH, MINB) fast_col_gs(FastArgs a, const __grid
             v[r] = mk(z.x, z.y);
         }
         float2* line = buf + c * LW;
-        fast_fft<N, TH, -1>(v, line, t, pt, tw);
+        if (!(a.debug & 1)) fast_fft<N, TH, -1>(v, line, t, pt, tw);
         float sdd = 0.f, srr = 0.f, srd = 0.f;
 #pragma unroll
         for (int r = 0; r < 16; ++r) {
@@ -585,11 +591,13 @@ __global__ void __launch_bounds__(TH, MINB) fast_col_gs(FastArgs a, const __grid
                 a.red.partials[3 * size_t(tile) + 2] = ts[2] * sc2;
             }
         }
-        fast_fft<N, TH, +1>(v, line, t, pt, tw);
+        if (!(a.debug & 1)) fast_fft<N, TH, +1>(v, line, t, pt, tw);
         float2* dst = a.data + size_t(tile) * C + c + size_t(t) * a.W;
         const size_t step = size_t(TF) * a.W;
+        if (!(a.debug & 2)) {
 #pragma unroll
-        for (int r = 0; r < 16; ++r) dst[r * step] = make_float2(v[r].x, v[r].y);
+            for (int r = 0; r < 16; ++r) dst[r * step] = make_float2(v[r].x, v[r].y);
+        }
         fence_proxy_async();
         __syncthreads();
         if (tid == 0) {
