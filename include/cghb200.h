@@ -214,6 +214,30 @@ int cgh_best_delta(int32_t device, const double *replay_m, const double *target_
                    const double *col_tw, const int32_t *mu, const int32_t *mv, int64_t count, int32_t h,
                    int32_t w, const double *deltas, int64_t levels, int64_t *best_index, double *best_change);
 
+/* ---- row-distributed GS slabs (config C6: one N x N run over G ranks) -----
+ * Replaces the pass loop of run_gs (algorithms.py:147-202) for one rank of a
+ * row-slab decomposition; the caller (paper_2006_10509_b200/slab.py) owns the
+ * device buffers and runs the all-to-all (NCCL) between passes on `stream`.
+ * A slab holds R = N/G lines as G segments of S = N/G points, segment-major:
+ * element (line i, position n) at ((n/S)*R + i)*S + n%S; block g (S*S
+ * elements) is the chunk exchanged with rank g. pb->height = pb->width = N
+ * (global). Pass modes: 0 random-phase init [-> snap] -> forward; 1 hologram
+ * pass (inverse -> beam*x/|x| [-> snap] -> forward); 2 replay pass (forward ->
+ * error sums + amplitude projection -> inverse); 3 final replay (sums only);
+ * 4 inverse (backpropagation start). Sums: 4 doubles {S_dd, S_rr, S_rd,
+ * S_all} of this rank written to the device pointer `sums` (modes 2, 3). */
+typedef struct cgh_slab cgh_slab;
+int cgh_slab_create(const cgh_problem *pb, int32_t world, int32_t rank, void *stream, cgh_slab **out);
+int cgh_slab_destroy(cgh_slab *slab);
+/* tgt_local: R x N float64, the ifftshifted |target| of this rank's columns
+ * (transposed), sign bit set outside the mask; beam_local: R x N |illumination|
+ * of this rank's hologram rows, or NULL. */
+int cgh_slab_set_local(cgh_slab *slab, const double *tgt_local, const double *beam_local);
+int cgh_slab_pass(cgh_slab *slab, int32_t mode, void *data, const cgh_gs_params *gp, int32_t quantize,
+                  void *idx_out, double *sums);
+/* dst[g] = transpose(src[g]) for every S x S block (the corner turn). */
+int cgh_slab_transpose(cgh_slab *slab, const void *src, void *dst);
+
 /* ---- host: materialise states[indices] as complex128 (the returned
  * hologram of every runner) with `threads` host threads (no GPU needed). */
 int cgh_expand_states(const void *idx, int32_t idx_bytes, int64_t count, const double *states, int32_t n_states,

@@ -558,7 +558,7 @@ __global__ void __launch_bounds__(TH, MINB) fast_col_gs(FastArgs a, const __grid
             v[r] = mk(z.x, z.y);
         }
         float2* line = buf + c * LW;
-        if (!(a.debug & 1)) fast_fft<N, TH, -1>(v, line, t, pt, tw);
+        fast_fft<N, TH, -1>(v, line, t, pt, tw);
         float sdd = 0.f, srr = 0.f, srd = 0.f;
 #pragma unroll
         for (int r = 0; r < 16; ++r) {
@@ -591,7 +591,7 @@ __global__ void __launch_bounds__(TH, MINB) fast_col_gs(FastArgs a, const __grid
                 a.red.partials[3 * size_t(tile) + 2] = ts[2] * sc2;
             }
         }
-        if (!(a.debug & 1)) fast_fft<N, TH, +1>(v, line, t, pt, tw);
+        fast_fft<N, TH, +1>(v, line, t, pt, tw);
         float2* dst = a.data + size_t(tile) * C + c + size_t(t) * a.W;
         const size_t step = size_t(TF) * a.W;
         if (!(a.debug & 2)) {

@@ -119,11 +119,10 @@ __device__ __forceinline__ int padx(int i) { return i + i / pad_unit<T>(); }
 template <class T, int N>
 __host__ __device__ constexpr int line_words() { return N + N / pad_unit<T>() + 1; }
 
-template <class T, int N, int DIR>
+template <class T, int N, int DIR, int EE = LineShape<T, N>::E>
 struct LineFft {
-    using Sh = LineShape<T, N>;
-    static constexpr int E = Sh::E;
-    static constexpr int TF = Sh::TF;
+    static constexpr int E = EE;   // elements per thread (default LineShape)
+    static constexpr int TF = N / E;
 
     template <int NS>
     __device__ __forceinline__ static void stages(cx<T> (&v)[E], T* sre, T* sim, int t, const cx<T>* __restrict__ tw) {

@@ -33,7 +33,7 @@ int fail(int code, const char* fmt, ...) {
 
 // ================================================================= tables
 // exp(-2 pi i k / n), k in [0, n), evaluated in long double.
-static void twiddle_table(int n, std::vector<double>& out) {
+void twiddle_table(int n, std::vector<double>& out) {
     out.resize(2 * size_t(n));
     const long double pi = 3.141592653589793238462643383279502884L;
     for (int k = 0; k < n; ++k) {
@@ -46,7 +46,7 @@ static void twiddle_table(int n, std::vector<double>& out) {
 // Separable Fresnel factor exp(i pi c^2 p^2 / (lambda z)), c = idx - n/2.
 // Product of the row and column factors equals fresnel_prefactor
 // (propagation.py:97-107) up to rounding of the reference's own fp64 argument.
-static void chirp_table(int n, double pitch, double wl, double dist, std::vector<double>& out) {
+void chirp_table(int n, double pitch, double wl, double dist, std::vector<double>& out) {
     out.resize(2 * size_t(n));
     const long double pi = 3.141592653589793238462643383279502884L;
     for (int k = 0; k < n; ++k) {

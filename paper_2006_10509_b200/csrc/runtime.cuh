@@ -86,6 +86,10 @@ struct cgh_plan {
 
 namespace cgh {
 
+// fp64 tables (long-double evaluation): exp(-2 pi i k / n); separable Fresnel chirp
+void twiddle_table(int n, std::vector<double>& out);
+void chirp_table(int n, double pitch, double wl, double dist, std::vector<double>& out);
+
 int plan_init(cgh_plan* P, const cgh_problem* pb);
 void plan_free(cgh_plan* P);
 int ensure(cgh_plan* P, DevBuf& b, size_t bytes);

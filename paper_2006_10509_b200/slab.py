@@ -1,0 +1,451 @@
+"""Row-distributed Gerchberg-Saxton for one large plane (config C6).
+
+One N x N run of ``run_gs`` (algorithms.py:147-202) split over G ranks (one
+process per GPU, ``torch.distributed`` over NCCL; or G virtual ranks driven
+from one process for tests). Rank r owns R = N/G lines of N points in the
+"segmented row" layout of ``csrc/slab_kernels.cuh``: a torch tensor of shape
+(G, R, R) whose block g is the chunk exchanged with rank g.
+
+Per iteration (both GS passes are row passes, each followed by a corner turn):
+
+    replay pass  (lines = original columns):  FFT -> error sums + amplitude projection -> IFFT
+    turn         block transpose + all_to_all_single
+    hologram pass (lines = original rows):    IFFT -> beam * x/|x| [-> snap] -> FFT
+    turn
+
+The start (random phase, row-major global draws) is a hologram pass; after the
+loop one replay pass computes the final error and efficiency. Per-iteration
+error sums stay on the device and are all-reduced once at the end (or every
+iteration when ``progress``/``cancel`` hooks need live values). Each line is
+transformed and projected with exactly the arithmetic of the single-GPU
+generic passes, so index planes equal ``run_gs``'s; only the summation order
+of the error sums differs.
+
+torch provides the device buffers, the stream and the collectives (plumbing);
+every pass and transpose is a kernel of ``libcghb200.so`` (``cgh_slab_*``).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+
+import numpy as np
+
+from . import _native
+from .algorithms import (
+    BACKPROPAGATE,
+    CANCELLED,
+    COMPLETED,
+    RANDOM_PHASE,
+    RunReport,
+    _check_inputs,
+    _init_code,
+    _mask_bytes,
+)
+from .errors import EmptyMaskError, NonFiniteError, UnsupportedShapeError, ZeroFieldError, ZeroTargetError
+from .propagation import fill_propagation
+from .runtime import current_device, runner_precision
+from .slm import problem_for, states
+
+SLAB_INIT, SLAB_HOLO, SLAB_GS, SLAB_FINAL, SLAB_INV = 0, 1, 2, 3, 4
+
+
+def error_from_sums(sdd, srr, srd, denom, rescale):
+    """Masked amplitude error from the four sums (passes.cuh error_from_sums,
+    propagation.py:164-192)."""
+    num = sdd
+    if rescale and srr > 0.0:
+        num = sdd - (srd * srd) / srr
+    return num / denom
+
+
+def local_inputs(cfg, target, illumination, world, rank):
+    """This rank's share of the prepared inputs (host, fp64):
+
+    * ``tgt``: R x N, ifftshifted |target| of columns [rR, (r+1)R), transposed,
+      sign bit set outside the ifftshifted mask (propagation.py:164-192 on the
+      uncentred replay plane);
+    * ``beam``: R x N |illumination| of hologram rows [rR, (r+1)R) or None;
+    * ``tcols``: R x N ifftshifted complex target columns (transposed), for
+      the backpropagation start;
+    * global statistics identical on every rank: count_in, denom = sum t^2
+      over the mask, non-finite counts.
+    """
+    n = target.shape[0]
+    r0, r1 = rank * (n // world), (rank + 1) * (n // world)
+    mask = np.fft.ifftshift(_mask_bytes(cfg, target) != 0)
+    tshift = np.fft.ifftshift(target)
+    amp = np.abs(tshift)
+    signed = np.where(mask, amp, -amp)
+    stats = {
+        "count_in": int(mask.sum()),
+        "denom": float(np.sum(amp[mask] ** 2)),
+        "nf_in": int(np.count_nonzero(~np.isfinite(tshift[mask]))),
+        "nf_all": int(np.count_nonzero(~np.isfinite(tshift))),
+        "nf_beam": 0 if illumination is None else int(np.count_nonzero(~np.isfinite(illumination))),
+    }
+    out = {
+        "tgt": np.ascontiguousarray(signed[:, r0:r1].T, dtype=np.float64),
+        "beam": None if illumination is None else np.ascontiguousarray(np.abs(illumination[r0:r1, :]), np.float64),
+        "tcols": np.ascontiguousarray(tshift[:, r0:r1].T),
+    }
+    return out, stats
+
+
+def to_segments(rows):
+    """(R, N) row-major lines -> (G, R, R) segmented slab (numpy or torch)."""
+    r, n = rows.shape
+    g = n // r
+    if isinstance(rows, np.ndarray):
+        return rows.reshape(r, g, r).transpose(1, 0, 2)
+    return rows.reshape(r, g, r).transpose(0, 1)
+
+
+def from_segments(seg):
+    """(G, R, R) segmented slab -> (R, N) row-major lines."""
+    g, r, _ = seg.shape
+    if isinstance(seg, np.ndarray):
+        return seg.transpose(1, 0, 2).reshape(r, g * r)
+    return seg.transpose(0, 1).reshape(r, g * r)
+
+
+# ------------------------------------------------------------------ exchanges
+
+
+class LocalExchange:
+    """G = 1: the corner turn is a plain transpose, no collective."""
+
+    world = 1
+
+    def all_to_all(self, sends, recvs):
+        raise AssertionError("no exchange at G = 1")
+
+    def all_reduce(self, tensors):
+        return tensors
+
+    def gather(self, tensors):
+        return tensors
+
+
+class TorchExchange:
+    """One rank of a torch.distributed group (NCCL on GPUs, gloo on CPU)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+
+    def all_to_all(self, sends, recvs):
+        import torch
+
+        (send,), (recv,) = sends, recvs
+        # complex slabs travel as (re, im) pairs: chunk g (R*R elements) -> rank g
+        self.dist.all_to_all_single(torch.view_as_real(recv), torch.view_as_real(send), group=self.group)
+
+    def all_reduce(self, tensors):
+        (t,) = tensors
+        self.dist.all_reduce(t, group=self.group)
+        return [t]
+
+    def gather(self, tensors):
+        import torch
+
+        (t,) = tensors
+        parts = [torch.empty_like(t) for _ in range(self.world)]
+        self.dist.all_gather(parts, t, group=self.group)
+        return parts
+
+
+class SimulatedExchange:
+    """G virtual ranks in one process on one device (tests): phases run rank
+    after rank, the all-to-all is block copies, so no kernel waits on another."""
+
+    def __init__(self, world):
+        self.world = world
+
+    def all_to_all(self, sends, recvs):
+        for h, recv in enumerate(recvs):
+            for g, send in enumerate(sends):
+                recv[g].copy_(send[h])
+
+    def all_reduce(self, tensors):
+        total = tensors[0].clone()
+        for t in tensors[1:]:
+            total += t
+        return [total.clone() for _ in tensors]
+
+    def gather(self, tensors):
+        return list(tensors)
+
+
+# ----------------------------------------------------------------- device ops
+
+
+class NativeOps:
+    """Slab passes and transposes through the C ABI (the product path)."""
+
+    def __init__(self, cfg, n, world, rank, precision, device, stream):
+        import torch
+
+        self.torch = torch
+        self.lib = _native.library()
+        _native.require_device()
+        self.pb, self._keep = problem_for(cfg.slm.scheme, n, n, precision, device)
+        fill_propagation(self.pb, cfg.propagation)
+        self.pb.rescale = 1 if cfg.metric.rescale else 0
+        self.handle = ctypes.c_void_p()
+        _native.check(self.lib.cgh_slab_create(ctypes.byref(self.pb), world, rank, ctypes.c_void_p(stream),
+                                               ctypes.byref(self.handle)))
+        self.device = torch.device("cuda", device)
+        self.cdtype = torch.complex128 if precision == _native.FP64 else torch.complex64
+        self.n_states = self.pb.n_states
+
+    def close(self):
+        if self.handle:
+            self.lib.cgh_slab_destroy(self.handle)
+            self.handle = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+    def empty(self, shape, kind="c"):
+        t = self.torch
+        dt = {"c": self.cdtype, "f64": t.float64, "idx": t.uint8 if self.n_states <= 256 else t.int32}[kind]
+        return t.empty(shape, dtype=dt, device=self.device)
+
+    def upload(self, arr, kind="c"):
+        return self.torch.from_numpy(np.ascontiguousarray(arr)).to(self.device, self.cdtype if kind == "c" else None)
+
+    def set_local(self, tgt, beam):
+        _native.check(self.lib.cgh_slab_set_local(self.handle, _native.ptr(tgt), _native.ptr(beam)))
+
+    def run(self, mode, data, gp=None, quantize=0, idx=None, sums=None):
+        _native.check(self.lib.cgh_slab_pass(
+            self.handle, mode, ctypes.c_void_p(data.data_ptr()), None if gp is None else ctypes.byref(gp),
+            1 if quantize else 0, None if idx is None else ctypes.c_void_p(idx.data_ptr()),
+            None if sums is None else ctypes.c_void_p(sums.data_ptr())))
+
+    def transpose(self, src, dst):
+        _native.check(self.lib.cgh_slab_transpose(self.handle, ctypes.c_void_p(src.data_ptr()),
+                                                  ctypes.c_void_p(dst.data_ptr())))
+
+    def sync(self):
+        self.torch.cuda.synchronize(self.device)
+
+
+_native_declared = False
+
+
+def _declare():
+    global _native_declared
+    if _native_declared:
+        return
+    lib = _native.library()
+    P, i32 = ctypes.c_void_p, ctypes.c_int32
+    pP = ctypes.POINTER
+    for name, args in {
+        "cgh_slab_create": [pP(_native.Problem), i32, i32, P, pP(P)],
+        "cgh_slab_destroy": [P],
+        "cgh_slab_set_local": [P, P, P],
+        "cgh_slab_pass": [P, i32, P, pP(_native.GsParams), i32, P, P],
+        "cgh_slab_transpose": [P, P, P],
+    }.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = ctypes.c_int
+    _native_declared = True
+
+
+# ------------------------------------------------------------------ one rank
+
+
+class SlabRank:
+    """Buffers and passes of one rank: A (hologram slab), C (replay slab),
+    B (send buffer), the local index plane and the per-iteration sums."""
+
+    def __init__(self, ops, world, n, iters):
+        self.ops = ops
+        self.G, self.N, self.R = world, n, n // world
+        shape = (world, self.R, self.R)
+        self.A = ops.empty(shape)
+        self.C = ops.empty(shape)
+        self.B = ops.empty(shape) if world > 1 else None
+        self.idx = ops.empty((self.R, n), "idx")
+        self.sums = ops.empty((iters + 1, 4), "f64")
+        self.sums.zero_()
+
+
+def _turn(ranks, exch, src, dst):
+    """Corner turn src -> dst on every rank (block transposes + all-to-all)."""
+    if exch.world == 1:
+        r = ranks[0]
+        r.ops.transpose(getattr(r, src), getattr(r, dst))
+        return
+    for r in ranks:
+        r.ops.transpose(getattr(r, src), r.B)
+    exch.all_to_all([r.B for r in ranks], [getattr(r, dst) for r in ranks])
+
+
+def _validate(stats, init_code, iters):
+    # the single-GPU runner's order (runtime.cu gs_exec)
+    if init_code == _native.INIT_BACKPROP and stats["nf_all"] > 0:
+        raise NonFiniteError("target contains NaN or Inf")
+    if stats["nf_beam"] > 0:
+        raise NonFiniteError("illumination contains NaN or Inf")
+    if stats["count_in"] == 0:
+        raise EmptyMaskError("metric mask has no true pixels")
+    if stats["denom"] == 0:
+        raise ZeroTargetError("target is zero inside the mask")
+    if stats["nf_in"] > 0 and iters > 0:
+        raise NonFiniteError("target contains NaN or Inf inside the mask")
+
+
+def drive(ranks, exch, cfg, local, gp, progress=None, cancel=None, stats=None):
+    """Run the GS iterations over the given ranks (one real rank, or all the
+    virtual ranks of a SimulatedExchange). Returns (sums (iters+1, 4) on the
+    host after the all-reduce, iterations executed, cancelled flag)."""
+    iters = max(0, int(cfg.iterations))
+    qe = bool(cfg.quantize_each_iteration)
+    init_code = _init_code(cfg.init_mode)
+    for r, loc in zip(ranks, local):
+        r.ops.set_local(loc["tgt"], loc["beam"])
+
+    def hologram_start(quantize):
+        if init_code == _native.INIT_RANDOM:
+            for r in ranks:
+                r.ops.run(SLAB_INIT, r.A, gp, quantize, r.idx if quantize else None)
+        else:   # backpropagate: ifftshift(T) -> inverse columns -> hologram pass
+            for r, loc in zip(ranks, local):
+                r.C.copy_(to_segments(r.ops.upload(loc["tcols"])))
+                r.ops.run(SLAB_INV, r.C, gp)
+            _turn(ranks, exch, "C", "A")
+            for r in ranks:
+                r.ops.run(SLAB_HOLO, r.A, gp, quantize, r.idx if quantize else None)
+        _turn(ranks, exch, "A", "C")
+
+    live = progress is not None or cancel is not None
+    hologram_start(iters == 0)
+    executed, stopped = 0, False
+    for k in range(iters):
+        if cancel is not None and _agree(exch, ranks, bool(cancel.is_set())):
+            stopped = True
+            break
+        for r in ranks:
+            r.ops.run(SLAB_GS, r.C, gp, sums=r.sums[k])
+        if live and progress is not None:
+            s = _reduced_row(exch, ranks, k)
+            progress(k, error_from_sums(s[0], s[1], s[2], stats["denom"], cfg.metric.rescale))
+        _turn(ranks, exch, "C", "A")
+        last = k == iters - 1
+        for r in ranks:
+            r.ops.run(SLAB_HOLO, r.A, gp, qe or last, r.idx if last else None)
+        _turn(ranks, exch, "A", "C")
+        executed = k + 1
+    if stopped:
+        if executed == 0:
+            hologram_start(True)
+        else:   # A still holds the last hologram pass output (the turn only reads it)
+            for r in ranks:
+                r.ops.run(SLAB_HOLO, r.A, gp, True, r.idx)
+            _turn(ranks, exch, "A", "C")
+    for r in ranks:
+        r.ops.run(SLAB_FINAL, r.C, gp, sums=r.sums[executed])
+    totals = exch.all_reduce([r.sums for r in ranks])
+    return totals[0].cpu().numpy(), executed, stopped
+
+
+def _agree(exch, ranks, flag):
+    """Cancel consensus: any rank's flag stops every rank."""
+    if exch.world == 1 or isinstance(exch, SimulatedExchange):
+        return flag
+    import torch
+
+    t = ranks[0].ops.empty((1,), "f64")
+    t.fill_(1.0 if flag else 0.0)
+    exch.all_reduce([t])
+    return bool(t.item() > 0)
+
+
+def _reduced_row(exch, ranks, k):
+    rows = [r.sums[k].clone() for r in ranks]
+    return exch.all_reduce(rows)[0].cpu().numpy()
+
+
+def run_gs_slab(cfg, target, illumination=None, progress=None, cancel=None, *, exchange=None, gather=True,
+                precision=None, device=None, ops_factory=None):
+    """``run_gs`` over a row-slab decomposition (drop-in signature plus the
+    distribution keywords). ``exchange``: None (G = 1), a ``TorchExchange``
+    (this process is one rank) or a ``SimulatedExchange`` (all ranks here).
+    Returns (hologram, RunReport): the full complex128 hologram when
+    ``gather`` (every rank), else this rank's rows (R x N)."""
+    start = time.perf_counter()
+    target = np.asarray(target, dtype=np.complex128)
+    _check_inputs(cfg, target, illumination)
+    init_code = _init_code(cfg.init_mode)
+    if cfg.init_mode not in (RANDOM_PHASE, BACKPROPAGATE):
+        raise ValueError(f"unknown init_mode {cfg.init_mode!r}")
+    h, w = target.shape
+    if h != w:
+        raise UnsupportedShapeError(f"slab runs need a square plane, got {target.shape}")
+    exch = exchange or LocalExchange()
+    world = exch.world
+    n = w
+    prec = runner_precision() if precision is None else precision
+    dev = current_device() if device is None else device
+    iters = max(0, int(cfg.iterations))
+    if isinstance(exch, SimulatedExchange):
+        rank_ids = list(range(world))
+    else:
+        rank_ids = [getattr(exch, "rank", 0)]
+    local, stats = [], None
+    for rk in rank_ids:
+        loc, stats = local_inputs(cfg, target, illumination, world, rk)
+        local.append(loc)
+    _validate(stats, init_code, iters)
+    if ops_factory is None:
+        import torch
+
+        _declare()
+        stream = torch.cuda.current_stream(dev).cuda_stream
+
+        def ops_factory(rk):
+            return NativeOps(cfg, n, world, rk, prec, dev, stream)
+
+    ranks = [SlabRank(ops_factory(rk), world, n, iters) for rk in rank_ids]
+    gp = _native.GsParams(iters, float(cfg.feedback_gain), 1 if cfg.quantize_each_iteration else 0, init_code,
+                          _native.Pcg64State.from_bitgen(np.random.PCG64(cfg.seed)))
+    sums, executed, stopped = drive(ranks, exch, cfg, local, gp, progress, cancel, stats)
+    denom, rescale = stats["denom"], bool(cfg.metric.rescale)
+    errs = [error_from_sums(s[0], s[1], s[2], denom, rescale) for s in sums[: executed + 1]]
+    s_fin = sums[executed]
+    if s_fin[3] == 0.0:
+        raise ZeroFieldError("replay field is zero")
+    eff = s_fin[1] / s_fin[3]
+    if progress is not None:
+        progress(executed, errs[executed])
+    if gather:
+        parts = exch.gather([r.idx for r in ranks])
+        idx = np.concatenate([p.cpu().numpy() for p in parts], axis=0)
+    else:
+        idx = np.concatenate([r.idx.cpu().numpy() for r in ranks], axis=0)
+    for r in ranks:
+        close = getattr(r.ops, "close", None)
+        if close:
+            close()
+    holo = _native.expand_states(idx, states(cfg.slm.scheme)) if hasattr(idx, "dtype") else idx
+    return holo, RunReport(
+        error_trace=[(k, float(e)) for k, e in enumerate(errs)],
+        final_error=float(errs[executed]),
+        efficiency=float(eff),
+        iterations_executed=int(executed),
+        runtime_ms=(time.perf_counter() - start) * 1e3,
+        seed_used=cfg.seed,
+        termination=CANCELLED if stopped else COMPLETED,
+    )
