@@ -38,6 +38,7 @@ EXPORTS = (
     "cgh_plan_download_idx", "cgh_plan_stream", "cgh_plan_sync", "cgh_plan_profile",
     "cgh_delta_error", "cgh_commit_update", "cgh_best_delta",
     "cgh_permutation", "cgh_random_doubles", "cgh_expand_states",
+    "cgh_slab_create", "cgh_slab_destroy", "cgh_slab_set_local", "cgh_slab_pass", "cgh_slab_transpose",
 )
 
 
@@ -155,6 +156,11 @@ def _declare(lib):
         "cgh_permutation": ([pP(Pcg64State), i64, P], ctypes.c_int),
         "cgh_expand_states": ([P, i32, i64, P, i32, P, i32], ctypes.c_int),
         "cgh_random_doubles": ([i32, pP(Pcg64State), i64, i64, P], ctypes.c_int),
+        "cgh_slab_create": ([pP(Problem), i32, i32, P, pP(P)], ctypes.c_int),
+        "cgh_slab_destroy": ([P], ctypes.c_int),
+        "cgh_slab_set_local": ([P, P, P], ctypes.c_int),
+        "cgh_slab_pass": ([P, i32, P, pP(GsParams), i32, P, P], ctypes.c_int),
+        "cgh_slab_transpose": ([P, P, P], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

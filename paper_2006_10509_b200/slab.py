@@ -240,29 +240,6 @@ class NativeOps:
         self.torch.cuda.synchronize(self.device)
 
 
-_native_declared = False
-
-
-def _declare():
-    global _native_declared
-    if _native_declared:
-        return
-    lib = _native.library()
-    P, i32 = ctypes.c_void_p, ctypes.c_int32
-    pP = ctypes.POINTER
-    for name, args in {
-        "cgh_slab_create": [pP(_native.Problem), i32, i32, P, pP(P)],
-        "cgh_slab_destroy": [P],
-        "cgh_slab_set_local": [P, P, P],
-        "cgh_slab_pass": [P, i32, P, pP(_native.GsParams), i32, P, P],
-        "cgh_slab_transpose": [P, P, P],
-    }.items():
-        fn = getattr(lib, name)
-        fn.argtypes = args
-        fn.restype = ctypes.c_int
-    _native_declared = True
-
-
 # ------------------------------------------------------------------ one rank
 
 
@@ -412,7 +389,6 @@ def run_gs_slab(cfg, target, illumination=None, progress=None, cancel=None, *, e
     if ops_factory is None:
         import torch
 
-        _declare()
         stream = torch.cuda.current_stream(dev).cuda_stream
 
         def ops_factory(rk):
