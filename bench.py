@@ -43,6 +43,8 @@ COL_BYTES_PER_PX = 20
 ROW_BYTES_PER_PX = 16
 OSPR_N = 1024
 OSPR_S = 24
+C5_N, C5_TARGETS, C5_ITERS = 4096, 64, 100   # batched GS (100 iterations)
+C6_N, C6_ITERS = 16384, 20                   # distributed GS (§8d: "C6 timing may use 20 iterations")
 METRIC = "GS iterations/s (Fresnel 2048x2048, PhaseOnly(8), 200 iterations per run)"
 
 
@@ -363,6 +365,86 @@ def run_ours(args):
                                     "dbs_pixels_per_s": "116 (BASELINE.md, survey container)"}}
         splan.close()
 
+    # C5: batched GS, targets 1..64 (seed = target id) in contiguous blocks per
+    # rank (multi.shard), a bounded sample of each rank's block timed
+    c5 = None
+    if not args.no_c5:
+        from paper_2006_10509_b200.multi import shard
+        from paper_2006_10509_b200.workloads import batched_target
+
+        lo, hi = shard(C5_TARGETS, world, rank)
+        mine = list(range(lo + 1, hi + 1))[: max(1, args.c5_sample)]
+        c5cfg = make_cfg(1, n=C5_N, kind="fourier", iterations=C5_ITERS)
+        c5plan = GenerationPlan(c5cfg, (C5_N, C5_N), precision=_native.FP32, device=local)
+        c5plan.set_target(batched_target(C5_N, mine[0]))
+        c5plan.gs(seed=mine[0], iterations=5)           # warm-up
+        gen_ms, e2e_s = [], 0.0
+        c5launch = 0
+        for tid in mine:
+            tgt = batched_target(C5_N, tid)              # host synthesis, not timed
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            c5plan.set_target(tgt)                       # H2D target + mask, device prep
+            rep5, _ = c5plan.gs(seed=tid)
+            c5plan.download_indices(1)                   # D2H index plane
+            e2e_s += time.perf_counter() - t0
+            gen_ms.append(rep5.device_ms)
+            c5launch += rep5.kernel_launches
+        barrier()
+        n_done = int(sum_over_ranks(len(mine)))
+        t5 = max_over_ranks(sum(gen_ms)) / 1000.0
+        te5 = max_over_ranks(e2e_s)
+        hw5 = C5_N * C5_N
+        it_ms = sum(gen_ms) / len(gen_ms) / C5_ITERS
+        c5 = {"metric": f"batched GS holograms/s ({C5_N}x{C5_N} Fourier PhaseOnly(8), {C5_ITERS} iterations, "
+                        f"targets 1..{C5_TARGETS} sharded over ranks)",
+              "value": n_done / t5, "unit": "holograms/s", "hologram_iterations_per_s": n_done * C5_ITERS / t5,
+              "scaling": "weak", "targets_timed": n_done,
+              "sample": f"first {len(mine)} target(s) of each rank's block of {hi - lo}",
+              "gpu_launches_per_hologram": c5launch / len(mine),
+              "e2e": {"value": n_done / te5, "unit": "holograms/s", "h2d_bytes_per_step": hw5 * 17,
+                      "d2h_bytes_per_step": hw5, "note": "set_target (complex128 target + mask) + GS + index download"},
+              "roofline": {"bound": "hbm", "achieved": GS_BYTES_PER_PX * hw5 / (it_ms / 1000.0) / 1e9, "peak": peak,
+                           "unit": "GB/s",
+                           "frac": GS_BYTES_PER_PX * hw5 / (it_ms / 1000.0) / 1e9 / peak,
+                           "algorithmic_bytes_per_iteration": GS_BYTES_PER_PX * hw5, "ms_per_iteration": it_ms}}
+        c5plan.close()
+
+    # C6: one 16384^2 GS plane over all ranks (row slabs, block-transpose corner
+    # turns, NCCL all_to_all_single between passes when N > 1)
+    c6 = None
+    if not args.no_c6:
+        from paper_2006_10509_b200 import slab as SL
+
+        c6cfg = make_cfg(1, n=C6_N, kind="fourier", iterations=C6_ITERS)
+        sess = SL.SlabSession(c6cfg, natural_target(C6_N), exchange=SL.TorchExchange() if world > 1 else None,
+                              precision=_native.FP32, device=local)
+        sess.run()                                       # warm-up
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c6ms = []
+        for _ in range(max(1, args.c6_steps)):
+            barrier()
+            ev0.record()
+            sums6, done6, _ = sess.run()
+            ev1.record()
+            torch.cuda.synchronize()
+            c6ms.append(ev0.elapsed_time(ev1))
+        t6 = max_over_ranks(sum(c6ms)) / 1000.0
+        err6 = sess.errors(sums6, done6)
+        sess.close()
+        hw6 = C6_N * C6_N
+        ms6 = max_over_ranks(sum(c6ms)) / len(c6ms) / C6_ITERS
+        c6 = {"metric": f"distributed GS iterations/s ({C6_N}x{C6_N} Fourier PhaseOnly(8), one plane over "
+                        f"{world} GPU(s), {C6_ITERS} iterations per run)",
+              "value": len(c6ms) * C6_ITERS / t6, "unit": "iter/s", "scaling": "strong", "ms_per_iteration": ms6,
+              "exchange": "nccl all_to_all_single" if world > 1 else "none (G = 1: block transpose only)",
+              "final_error": err6[-1],
+              "roofline": {"bound": "hbm", "achieved": GS_BYTES_PER_PX * hw6 / (ms6 / 1000.0) / 1e9 / world,
+                           "peak": peak, "unit": "GB/s (per GPU)",
+                           "frac": GS_BYTES_PER_PX * hw6 / (ms6 / 1000.0) / 1e9 / world / peak,
+                           "algorithmic_bytes_per_iteration": GS_BYTES_PER_PX * hw6,
+                           "note": "36 B/px algorithmic; the design also moves 2 x 16 B/px of corner turns"}}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline_gs()
@@ -377,7 +459,7 @@ def run_ours(args):
                            "l2": "256 MB device write between timed steps (excluded from step time)"},
                 "gpu_launches": launches, "wall_s_timed": t_wall,
                 "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clk.summary(), "ospr": ospr,
-                "search": search}
+                "search": search, "c5": c5, "c6": c6}
         print(json.dumps(line), flush=True)
     plan.close()
     if world > 1:
@@ -394,6 +476,10 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-ospr", action="store_true")
     ap.add_argument("--no-search", action="store_true")
+    ap.add_argument("--no-c5", action="store_true")
+    ap.add_argument("--no-c6", action="store_true")
+    ap.add_argument("--c5-sample", type=int, default=8, help="targets timed per rank (of its block of 64/N)")
+    ap.add_argument("--c6-steps", type=int, default=3)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

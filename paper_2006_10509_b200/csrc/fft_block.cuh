@@ -103,6 +103,25 @@ struct Dft<32, DIR, S, T> {
 // --------------------------------------------------------------- line FFT
 __host__ __device__ constexpr int ilog2(int n) { return n <= 1 ? 0 : 1 + ilog2(n / 2); }
 
+// Twiddle sources: the N-entry global table tw[k] = exp(-2 pi i k / N), or a
+// two-level shared-memory table (w^k = hi[k >> sh] * lo[k & (2^sh - 1)], two
+// tables of sqrt(N) entries; one extra rounding) for long lines whose N-entry
+// table does not stay in L1.
+template <class T>
+struct TwSplit {
+    const cx<T>* hi;
+    const cx<T>* lo;
+    int sh;
+};
+template <class T>
+__device__ __forceinline__ cx<T> tw_at(const cx<T>* __restrict__ tw, int k) {
+    return ldg_cx(tw + k);
+}
+template <class T>
+__device__ __forceinline__ cx<T> tw_at(const TwSplit<T>& s, int k) {
+    return cmul(s.hi[k >> s.sh], s.lo[k & ((1 << s.sh) - 1)]);
+}
+
 // Elements per thread for a line of N points at precision T.
 template <class T, int N>
 struct LineShape {
@@ -124,8 +143,8 @@ struct LineFft {
     static constexpr int E = EE;   // elements per thread (default LineShape)
     static constexpr int TF = N / E;
 
-    template <int NS>
-    __device__ __forceinline__ static void stages(cx<T> (&v)[E], T* sre, T* sim, int t, const cx<T>* __restrict__ tw) {
+    template <int NS, class TWS>
+    __device__ __forceinline__ static void stages(cx<T> (&v)[E], T* sre, T* sim, int t, const TWS& tw) {
         constexpr int R = (N / NS >= E) ? E : N / NS;
         constexpr int NB = E / R;
         // v[b*R + r] = x_s[j + r*N/R], j = t + b*TF
@@ -136,7 +155,7 @@ struct LineFft {
                 const int jm = j & (NS - 1);
 #pragma unroll
                 for (int r = 1; r < R; ++r) {
-                    cx<T> w = ldg_cx(tw + jm * r * (N / (NS * R)));
+                    cx<T> w = tw_at<T>(tw, jm * r * (N / (NS * R)));
                     v[b * R + r] = DIR < 0 ? cmul(v[b * R + r], w) : cmulc(v[b * R + r], w);
                 }
             }
@@ -184,6 +203,9 @@ struct LineFft {
 
     // Transform one line held in strided-natural layout (unscaled).
     __device__ __forceinline__ static void run(cx<T> (&v)[E], T* sre, T* sim, int t, const cx<T>* __restrict__ tw) {
+        stages<1>(v, sre, sim, t, tw);
+    }
+    __device__ __forceinline__ static void run(cx<T> (&v)[E], T* sre, T* sim, int t, const TwSplit<T>& tw) {
         stages<1>(v, sre, sim, t, tw);
     }
 };

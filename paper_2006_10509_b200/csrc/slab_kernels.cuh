@@ -15,6 +15,9 @@
 // planes equal the single-GPU generic path bit for bit; only the order of the
 // error sums differs (per-rank block sums, all-reduced once per run).
 #pragma once
+#include <algorithm>
+#include <type_traits>
+
 #include "pass_kernels.cuh"
 
 namespace cgh {
@@ -36,7 +39,14 @@ struct SlabShape {
     static constexpr int THREADS = TF >= 256 ? TF : 256;
     static constexpr int LINES = THREADS / TF;
     static constexpr int WORDS = line_words<T, N>();
-    static constexpr size_t SMEM = size_t(LINES) * 2 * WORDS * sizeof(T) + 16 + 32 * 4 * sizeof(double);
+    // fp32: two-level twiddle table in shared memory (fp64 parity mode keeps
+    // the exact N-entry table of the generic passes)
+    static constexpr bool SPLIT_TW = sizeof(T) == 4 && N >= 1024;
+    static constexpr int TW_SH = (ilog2(N) + 1) / 2;
+    static constexpr int TW_WORDS = SPLIT_TW ? ((N >> TW_SH) + (1 << TW_SH)) : 0;
+    static constexpr size_t FFT_BYTES = size_t(LINES) * 2 * WORDS * sizeof(T);
+    static constexpr size_t TW_OFF = (FFT_BYTES + 16 + 32 * 4 * sizeof(double) + 15) / 16 * 16;
+    static constexpr size_t SMEM = TW_OFF + size_t(TW_WORDS) * sizeof(cx<T>);
 };
 
 template <class T>
@@ -51,132 +61,180 @@ struct SlabArgs {
     ReduceArgs red;       // out[0..3] = S_dd, S_rr, S_rd, S_all of this rank
 };
 
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+template <class T, int N, int DIR>
+__device__ __forceinline__ void slab_fft(cx<T> (&v)[SlabShape<T, N>::E], T* sre, T* sim, int t,
+                                         const unsigned char* smem, const cx<T>* tw) {
+    using Sh = SlabShape<T, N>;
+    if constexpr (Sh::SPLIT_TW) {
+        const cx<T>* tws = reinterpret_cast<const cx<T>*>(smem + Sh::TW_OFF);
+        LineFft<T, N, DIR, Sh::E>::run(v, sre, sim, t, TwSplit<T>{tws, tws + (N >> Sh::TW_SH), Sh::TW_SH});
+    } else {
+        LineFft<T, N, DIR, Sh::E>::run(v, sre, sim, t, tw);
+    }
+}
+
+// Persistent: CTA b transforms line groups b, b + gridDim.x, ... and asks L2
+// for its next group (all segments, and the target / beam rows) before
+// working on the current one, so the next loads hit L2 instead of HBM.
 template <class T, int N, int MODE>
 __global__ void __launch_bounds__(SlabShape<T, N>::THREADS) slab_kernel(SlabArgs<T> a) {
-    constexpr int mode = MODE;
     using Sh = SlabShape<T, N>;
+    constexpr int mode = MODE;
     constexpr int E = Sh::E, TF = Sh::TF, WORDS = Sh::WORDS;
     extern __shared__ __align__(16) unsigned char smem[];
     const int li = threadIdx.x / TF, t = threadIdx.x - li * TF;
-    const int i = blockIdx.x * Sh::LINES + li;
-    const bool active = i < a.R;
     T* sre = reinterpret_cast<T*>(smem) + li * 2 * WORDS;
     T* sim = sre + WORDS;
-    double* rs = red_scratch<T>(smem, size_t(Sh::LINES) * 2 * WORDS * sizeof(T));
+    double* rs = red_scratch<T>(smem, Sh::FFT_BYTES);
     const int S = 1 << a.logS;
-    auto at = [&](int n) -> long { return (long((n >> a.logS)) * a.R + i) * S + (n & (S - 1)); };
-    cx<T> v[E];
+    const int G = N >> a.logS;
 
-    if constexpr (mode == SLAB_INIT) {
-        // thread t draws the contiguous chunk [t*E, t*E+E) of global row line0+i
-        // (row-major over the full plane, algorithms.py:132), staged through smem
-        if (active) {
-            Pcg64 g = a.rng;
-            pcg_advance(g, uint64_t(long(a.line0 + i) * N + long(t) * E));
-#pragma unroll 4
-            for (int e = 0; e < E; ++e) {
-                const cx<T> z = unit_phase<T>(g);
-                const int pos = t * E + e;
-                const T amp = a.p.beam ? a.p.beam[long(i) * N + pos] : T(1);
-                const int q = padx<T>(pos);
-                sre[q] = amp * z.x;
-                sim[q] = amp * z.y;
+    if constexpr (Sh::SPLIT_TW) {
+        cx<T>* tws = reinterpret_cast<cx<T>*>(smem + Sh::TW_OFF);
+        constexpr int NH = N >> Sh::TW_SH, NL = 1 << Sh::TW_SH;
+        for (int k = threadIdx.x; k < NH + NL; k += blockDim.x)
+            tws[k] = k < NH ? ldg_cx(a.p.tw_row + (k << Sh::TW_SH)) : ldg_cx(a.p.tw_row + (k - NH));
+    }
+    double dsdd = 0, dsrr = 0, dsrd = 0, dsall = 0;   // SLAB_GS / SLAB_FINAL sums over this CTA's lines
+
+    for (int base = blockIdx.x * Sh::LINES; base < a.R; base += gridDim.x * Sh::LINES) {
+        const int i = base + li;
+        const bool active = i < a.R;
+        auto at = [&](int n) -> long { return (long((n >> a.logS)) * a.R + i) * S + (n & (S - 1)); };
+        {   // L2 prefetch of the next line group of this CTA
+            const int nb = base + gridDim.x * Sh::LINES;
+            const int k = threadIdx.x;
+            if (k < Sh::LINES * G && nb + k / G < a.R) {
+                const int ni = nb + k / G, g = k % G;
+                if (mode != SLAB_INIT) prefetch_l2(a.data + (long(g) * a.R + ni) * S, uint32_t(S) * sizeof(cx<T>));
+                if (g == 0 && (mode == SLAB_GS || mode == SLAB_FINAL)) prefetch_l2(a.tgt + long(ni) * N, N * sizeof(T));
+                if (g == 0 && (mode == SLAB_INIT || mode == SLAB_HOLO) && a.p.beam)
+                    prefetch_l2(a.p.beam + long(ni) * N, N * sizeof(T));
             }
         }
-        __syncthreads();
-#pragma unroll
-        for (int r = 0; r < E; ++r) {
-            const int q = padx<T>(t + r * TF);
-            v[r] = mk(sre[q], sim[q]);
-        }
-        if (active) {
-            const bool fres = a.p.q_row != nullptr;
-#pragma unroll
-            for (int r = 0; r < E; ++r) {
-                const int n = t + r * TF;
-                cx<T> h = v[r];
-                if (a.p.quantize) {
-                    const int k = quantize_index<T>(a.p.scheme, h);
-                    if (a.p.idx_out) {
-                        const long q = long(i) * N + n;
-                        if (a.p.idx_bytes == 1) static_cast<uint8_t*>(a.p.idx_out)[q] = (uint8_t)k;
-                        else static_cast<int32_t*>(a.p.idx_out)[q] = k;
-                    }
-                    h = state_value<T>(a.p.scheme, k);
-                }
-                if (fres) h = cmul(h, cmul(a.p.q_row[i], a.p.q_col[n]));
-                v[r] = h;
-            }
-        }
-        LineFft<T, N, -1, E>::run(v, sre, sim, t, a.p.tw_row);
-    } else {
-#pragma unroll
-        for (int r = 0; r < E; ++r) v[r] = active ? a.data[at(t + r * TF)] : mk<T>(0, 0);
-        if constexpr (mode == SLAB_HOLO) {
-            LineFft<T, N, +1, E>::run(v, sre, sim, t, a.p.tw_row);
+        __syncthreads();   // shared line buffers / twiddles ready, previous line done
+        cx<T> v[E];
+
+        if constexpr (mode == SLAB_INIT) {
+            // thread t draws the contiguous chunk [t*E, t*E+E) of global row line0+i
+            // (row-major over the full plane, algorithms.py:132), staged through smem
             if (active) {
-#pragma unroll
-                for (int r = 0; r < E; ++r) v[r] = holo_project<T>(a.p, v[r], i, t + r * TF, 0);
+                Pcg64 g = a.rng;
+                pcg_advance(g, uint64_t(long(a.line0 + i) * N + long(t) * E));
+#pragma unroll 4
+                for (int e = 0; e < E; ++e) {
+                    const cx<T> z = unit_phase<T>(g);
+                    const int pos = t * E + e;
+                    const T amp = a.p.beam ? a.p.beam[long(i) * N + pos] : T(1);
+                    const int q = padx<T>(pos);
+                    sre[q] = amp * z.x;
+                    sim[q] = amp * z.y;
+                }
             }
-            LineFft<T, N, -1, E>::run(v, sre, sim, t, a.p.tw_row);
-        } else if constexpr (mode == SLAB_INV) {
-            LineFft<T, N, +1, E>::run(v, sre, sim, t, a.p.tw_row);
-#pragma unroll
-            for (int r = 0; r < E; ++r) v[r] = v[r] * a.scale;
-        } else {   // SLAB_GS, SLAB_FINAL (pass_kernels.cuh COL_GS / COL_FINAL per line)
-            LineFft<T, N, -1, E>::run(v, sre, sim, t, a.p.tw_row);
-            T sdd = 0, srr = 0, srd = 0, sall = 0;
-            const T gain = a.gain;
+            __syncthreads();
 #pragma unroll
             for (int r = 0; r < E; ++r) {
-                const int u = t + r * TF;
-                const cx<T> Rv = v[r] * a.scale;
-                const T r2 = Rv.x * Rv.x + Rv.y * Rv.y;
-                const T rr = dev_sqrt<T>(r2);
-                const T tt = active ? a.tgt[long(i) * N + u] : T(-0.0);
-                sall += active ? r2 : T(0);
-                cx<T> out = Rv;
-                if (!signbit(tt)) {
-                    const T d = rr - tt;
-                    sdd += d * d;
-                    srr += r2;
-                    srd += rr * d;
-                    if constexpr (mode == SLAB_GS) {
-                        T want = tt + gain * (tt - rr);
-                        want = want > T(0) ? want : T(0);
-                        if (rr > T(0)) {
-                            const T s = want / rr;
-                            out = mk(Rv.x * s, Rv.y * s);
-                        } else {
-                            out = mk(want, T(0));
+                const int q = padx<T>(t + r * TF);
+                v[r] = mk(sre[q], sim[q]);
+            }
+            if (active) {
+                const bool fres = a.p.q_row != nullptr;
+#pragma unroll
+                for (int r = 0; r < E; ++r) {
+                    const int n = t + r * TF;
+                    cx<T> h = v[r];
+                    if (a.p.quantize) {
+                        const int k = quantize_index<T>(a.p.scheme, h);
+                        if (a.p.idx_out) {
+                            const long q = long(i) * N + n;
+                            if (a.p.idx_bytes == 1) static_cast<uint8_t*>(a.p.idx_out)[q] = (uint8_t)k;
+                            else static_cast<int32_t*>(a.p.idx_out)[q] = k;
+                        }
+                        h = state_value<T>(a.p.scheme, k);
+                    }
+                    if (fres) h = cmul(h, cmul(a.p.q_row[i], a.p.q_col[n]));
+                    v[r] = h;
+                }
+            }
+            slab_fft<T, N, -1>(v, sre, sim, t, smem, a.p.tw_row);
+        } else {
+#pragma unroll
+            for (int r = 0; r < E; ++r) v[r] = active ? a.data[at(t + r * TF)] : mk<T>(0, 0);
+            if constexpr (mode == SLAB_HOLO) {
+                slab_fft<T, N, +1>(v, sre, sim, t, smem, a.p.tw_row);
+                if (active) {
+#pragma unroll
+                    for (int r = 0; r < E; ++r) v[r] = holo_project<T>(a.p, v[r], i, t + r * TF, 0);
+                }
+                slab_fft<T, N, -1>(v, sre, sim, t, smem, a.p.tw_row);
+            } else if constexpr (mode == SLAB_INV) {
+                slab_fft<T, N, +1>(v, sre, sim, t, smem, a.p.tw_row);
+#pragma unroll
+                for (int r = 0; r < E; ++r) v[r] = v[r] * a.scale;
+            } else {   // SLAB_GS, SLAB_FINAL (pass_kernels.cuh COL_GS / COL_FINAL per line)
+                slab_fft<T, N, -1>(v, sre, sim, t, smem, a.p.tw_row);
+                const T gain = a.gain;
+                T sdd = 0, srr = 0, srd = 0, sall = 0;
+#pragma unroll
+                for (int r = 0; r < E; ++r) {
+                    const int u = t + r * TF;
+                    const cx<T> Rv = v[r] * a.scale;
+                    const T r2 = Rv.x * Rv.x + Rv.y * Rv.y;
+                    const T rr = dev_sqrt<T>(r2);
+                    const T tt = active ? a.tgt[long(i) * N + u] : T(-0.0);
+                    sall += active ? r2 : T(0);
+                    cx<T> out = Rv;
+                    if (!signbit(tt)) {
+                        const T d = rr - tt;
+                        sdd += d * d;
+                        srr += r2;
+                        srd += rr * d;
+                        if constexpr (mode == SLAB_GS) {
+                            T want = tt + gain * (tt - rr);
+                            want = want > T(0) ? want : T(0);
+                            if (rr > T(0)) {
+                                const T s = want / rr;
+                                out = mk(Rv.x * s, Rv.y * s);
+                            } else {
+                                out = mk(want, T(0));
+                            }
                         }
                     }
+                    v[r] = out;
                 }
-                v[r] = out;
+                dsdd += double(sdd);
+                dsrr += double(srr);
+                dsrd += double(srd);
+                dsall += double(sall);
+                if constexpr (mode == SLAB_GS) slab_fft<T, N, +1>(v, sre, sim, t, smem, a.p.tw_row);
             }
-            if constexpr (mode == SLAB_GS) LineFft<T, N, +1, E>::run(v, sre, sim, t, a.p.tw_row);
-            double acc[4] = {double(sdd), double(srr), double(srd), double(sall)};
-            block_reduce<4>(acc, rs);
-            const int nblocks = gridDim.x;
-            if (publish_partials<4>(a.red, acc, nblocks, blockIdx.x)) {
-                const double s0 = sum_partials(a.red, 0, nblocks, rs);
-                const double s1 = sum_partials(a.red, 1, nblocks, rs);
-                const double s2 = sum_partials(a.red, 2, nblocks, rs);
-                const double s3 = sum_partials(a.red, 3, nblocks, rs);
-                if (threadIdx.x == 0) {
-                    a.red.out[0] = s0;
-                    a.red.out[1] = s1;
-                    a.red.out[2] = s2;
-                    a.red.out[3] = s3;
-                    *a.red.counter = 0u;
-                }
-            }
-            if constexpr (mode == SLAB_FINAL) return;
+        }
+        if (mode != SLAB_FINAL && active) {
+#pragma unroll
+            for (int r = 0; r < E; ++r) a.data[at(t + r * TF)] = v[r];
         }
     }
-    if (active) {
-#pragma unroll
-        for (int r = 0; r < E; ++r) a.data[at(t + r * TF)] = v[r];
+    if constexpr (mode == SLAB_GS || mode == SLAB_FINAL) {
+        double acc[4] = {dsdd, dsrr, dsrd, dsall};
+        block_reduce<4>(acc, rs);
+        const int nblocks = gridDim.x;
+        if (publish_partials<4>(a.red, acc, nblocks, blockIdx.x)) {
+            const double s0 = sum_partials(a.red, 0, nblocks, rs);
+            const double s1 = sum_partials(a.red, 1, nblocks, rs);
+            const double s2 = sum_partials(a.red, 2, nblocks, rs);
+            const double s3 = sum_partials(a.red, 3, nblocks, rs);
+            if (threadIdx.x == 0) {
+                a.red.out[0] = s0;
+                a.red.out[1] = s1;
+                a.red.out[2] = s2;
+                a.red.out[3] = s3;
+                *a.red.counter = 0u;
+            }
+        }
     }
 }
 
@@ -209,7 +267,15 @@ cudaError_t slab_launch_m(const SlabArgs<T>& a, cudaStream_t st) {
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    const int grid = (a.R + Sh::LINES - 1) / Sh::LINES;
+    static int resident = 0;   // persistent grid: CTAs resident at once, capped by the line groups
+    if (!resident) {
+        int dev = 0, sms = 0, per = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, slab_kernel<T, N, MODE>, Sh::THREADS, Sh::SMEM);
+        resident = std::max(1, sms * std::max(1, per));
+    }
+    const int grid = std::min(resident, (a.R + Sh::LINES - 1) / Sh::LINES);
     slab_kernel<T, N, MODE><<<grid, Sh::THREADS, Sh::SMEM, st>>>(a);
     return cudaGetLastError();
 }

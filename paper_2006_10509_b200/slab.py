@@ -60,7 +60,7 @@ def error_from_sums(sdd, srr, srd, denom, rescale):
     return num / denom
 
 
-def local_inputs(cfg, target, illumination, world, rank):
+def local_inputs(cfg, target, illumination, world, rank, chunk_rows=1024):
     """This rank's share of the prepared inputs (host, fp64):
 
     * ``tgt``: R x N, ifftshifted |target| of columns [rR, (r+1)R), transposed,
@@ -70,25 +70,45 @@ def local_inputs(cfg, target, illumination, world, rank):
     * ``tcols``: R x N ifftshifted complex target columns (transposed), for
       the backpropagation start;
     * global statistics identical on every rank: count_in, denom = sum t^2
-      over the mask, non-finite counts.
+      over the mask, non-finite counts (accumulated over row chunks, so a
+      16384^2 plane never needs a full-size temporary).
+
+    ifftshift of an even-sized axis is a roll by -N/2, so shifted column v is
+    original column (v + N/2) mod N and shifted row u is original row
+    (u + N/2) mod N.
     """
     n = target.shape[0]
-    r0, r1 = rank * (n // world), (rank + 1) * (n // world)
-    mask = np.fft.ifftshift(_mask_bytes(cfg, target) != 0)
-    tshift = np.fft.ifftshift(target)
-    amp = np.abs(tshift)
-    signed = np.where(mask, amp, -amp)
+    rr = n // world
+    r0 = rank * rr
+    half = n // 2
+    mask = np.asarray(cfg.metric.mask)
+    if mask.shape != target.shape:
+        _mask_bytes(cfg, target)   # raises DimensionMismatchError
+    cols = (np.arange(r0, r0 + rr) + half) % n
+    tcols = np.roll(target[:, cols], -half, axis=0)            # (N, R) = ifftshift(T)[:, r0:r0+R]
+    mcols = np.roll(mask[:, cols] != 0, -half, axis=0)
+    amp = np.abs(tcols)
+    signed = np.where(mcols, amp, -amp)
+    count_in, denom, nf_in, nf_all = 0, 0.0, 0, 0
+    for a in range(0, n, chunk_rows):
+        t = target[a:a + chunk_rows]
+        m = mask[a:a + chunk_rows] != 0
+        fin = np.isfinite(t)
+        count_in += int(m.sum())
+        denom += float(np.sum(np.abs(t[m]) ** 2))
+        nf_in += int(np.count_nonzero(~fin & m))
+        nf_all += int(np.count_nonzero(~fin))
     stats = {
-        "count_in": int(mask.sum()),
-        "denom": float(np.sum(amp[mask] ** 2)),
-        "nf_in": int(np.count_nonzero(~np.isfinite(tshift[mask]))),
-        "nf_all": int(np.count_nonzero(~np.isfinite(tshift))),
+        "count_in": count_in,
+        "denom": denom,
+        "nf_in": nf_in,
+        "nf_all": nf_all,
         "nf_beam": 0 if illumination is None else int(np.count_nonzero(~np.isfinite(illumination))),
     }
     out = {
-        "tgt": np.ascontiguousarray(signed[:, r0:r1].T, dtype=np.float64),
-        "beam": None if illumination is None else np.ascontiguousarray(np.abs(illumination[r0:r1, :]), np.float64),
-        "tcols": np.ascontiguousarray(tshift[:, r0:r1].T),
+        "tgt": np.ascontiguousarray(signed.T, dtype=np.float64),
+        "beam": None if illumination is None else np.ascontiguousarray(np.abs(illumination[r0:r0 + rr, :]), np.float64),
+        "tcols": np.ascontiguousarray(tcols.T),
     }
     return out, stats
 
@@ -291,8 +311,6 @@ def drive(ranks, exch, cfg, local, gp, progress=None, cancel=None, stats=None):
     iters = max(0, int(cfg.iterations))
     qe = bool(cfg.quantize_each_iteration)
     init_code = _init_code(cfg.init_mode)
-    for r, loc in zip(ranks, local):
-        r.ops.set_local(loc["tgt"], loc["beam"])
 
     def hologram_start(quantize):
         if init_code == _native.INIT_RANDOM:
@@ -355,67 +373,94 @@ def _reduced_row(exch, ranks, k):
     return exch.all_reduce(rows)[0].cpu().numpy()
 
 
+class SlabSession:
+    """Prepared distributed GS run: inputs partitioned and uploaded once, then
+    ``run()`` repeatedly (benchmarks; the device work per run is the whole
+    iteration loop). ``exchange``: None (G = 1), a ``TorchExchange`` (this
+    process is one rank) or a ``SimulatedExchange`` (all ranks here)."""
+
+    def __init__(self, cfg, target, illumination=None, *, exchange=None, precision=None, device=None,
+                 ops_factory=None):
+        target = np.asarray(target, dtype=np.complex128)
+        _check_inputs(cfg, target, illumination)
+        if cfg.init_mode not in (RANDOM_PHASE, BACKPROPAGATE):
+            raise ValueError(f"unknown init_mode {cfg.init_mode!r}")
+        self.init_code = _init_code(cfg.init_mode)
+        h, w = target.shape
+        if h != w:
+            raise UnsupportedShapeError(f"slab runs need a square plane, got {target.shape}")
+        self.cfg = cfg
+        self.exch = exchange or LocalExchange()
+        world = self.exch.world
+        self.n = n = w
+        self.iters = max(0, int(cfg.iterations))
+        prec = runner_precision() if precision is None else precision
+        dev = current_device() if device is None else device
+        rank_ids = list(range(world)) if isinstance(self.exch, SimulatedExchange) else [getattr(self.exch, "rank", 0)]
+        self.local, stats = [], None
+        for rk in rank_ids:
+            loc, stats = local_inputs(cfg, target, illumination, world, rk)
+            self.local.append(loc)
+        self.stats = stats
+        _validate(stats, self.init_code, self.iters)
+        if ops_factory is None:
+            import torch
+
+            stream = torch.cuda.current_stream(dev).cuda_stream
+
+            def ops_factory(rk):
+                return NativeOps(cfg, n, world, rk, prec, dev, stream)
+
+        self.ranks = [SlabRank(ops_factory(rk), world, n, self.iters) for rk in rank_ids]
+        for r, loc in zip(self.ranks, self.local):
+            r.ops.set_local(loc["tgt"], loc["beam"])
+
+    def run(self, seed=None, progress=None, cancel=None):
+        """One generation; returns (sums (iters+1, 4), executed, cancelled)."""
+        cfg = self.cfg
+        gp = _native.GsParams(self.iters, float(cfg.feedback_gain), 1 if cfg.quantize_each_iteration else 0,
+                              self.init_code,
+                              _native.Pcg64State.from_bitgen(np.random.PCG64(cfg.seed if seed is None else seed)))
+        return drive(self.ranks, self.exch, cfg, self.local, gp, progress, cancel, self.stats)
+
+    def errors(self, sums, executed):
+        denom, rescale = self.stats["denom"], bool(self.cfg.metric.rescale)
+        return [error_from_sums(s[0], s[1], s[2], denom, rescale) for s in sums[: executed + 1]]
+
+    def indices(self, gather=True):
+        if gather:
+            parts = self.exch.gather([r.idx for r in self.ranks])
+            return np.concatenate([p.cpu().numpy() for p in parts], axis=0)
+        return np.concatenate([r.idx.cpu().numpy() for r in self.ranks], axis=0)
+
+    def close(self):
+        for r in self.ranks:
+            close = getattr(r.ops, "close", None)
+            if close:
+                close()
+
+
 def run_gs_slab(cfg, target, illumination=None, progress=None, cancel=None, *, exchange=None, gather=True,
                 precision=None, device=None, ops_factory=None):
     """``run_gs`` over a row-slab decomposition (drop-in signature plus the
-    distribution keywords). ``exchange``: None (G = 1), a ``TorchExchange``
-    (this process is one rank) or a ``SimulatedExchange`` (all ranks here).
-    Returns (hologram, RunReport): the full complex128 hologram when
-    ``gather`` (every rank), else this rank's rows (R x N)."""
+    distribution keywords). Returns (hologram, RunReport): the full complex128
+    hologram when ``gather`` (every rank), else this rank's rows (R x N)."""
     start = time.perf_counter()
-    target = np.asarray(target, dtype=np.complex128)
-    _check_inputs(cfg, target, illumination)
-    init_code = _init_code(cfg.init_mode)
-    if cfg.init_mode not in (RANDOM_PHASE, BACKPROPAGATE):
-        raise ValueError(f"unknown init_mode {cfg.init_mode!r}")
-    h, w = target.shape
-    if h != w:
-        raise UnsupportedShapeError(f"slab runs need a square plane, got {target.shape}")
-    exch = exchange or LocalExchange()
-    world = exch.world
-    n = w
-    prec = runner_precision() if precision is None else precision
-    dev = current_device() if device is None else device
-    iters = max(0, int(cfg.iterations))
-    if isinstance(exch, SimulatedExchange):
-        rank_ids = list(range(world))
-    else:
-        rank_ids = [getattr(exch, "rank", 0)]
-    local, stats = [], None
-    for rk in rank_ids:
-        loc, stats = local_inputs(cfg, target, illumination, world, rk)
-        local.append(loc)
-    _validate(stats, init_code, iters)
-    if ops_factory is None:
-        import torch
-
-        stream = torch.cuda.current_stream(dev).cuda_stream
-
-        def ops_factory(rk):
-            return NativeOps(cfg, n, world, rk, prec, dev, stream)
-
-    ranks = [SlabRank(ops_factory(rk), world, n, iters) for rk in rank_ids]
-    gp = _native.GsParams(iters, float(cfg.feedback_gain), 1 if cfg.quantize_each_iteration else 0, init_code,
-                          _native.Pcg64State.from_bitgen(np.random.PCG64(cfg.seed)))
-    sums, executed, stopped = drive(ranks, exch, cfg, local, gp, progress, cancel, stats)
-    denom, rescale = stats["denom"], bool(cfg.metric.rescale)
-    errs = [error_from_sums(s[0], s[1], s[2], denom, rescale) for s in sums[: executed + 1]]
-    s_fin = sums[executed]
-    if s_fin[3] == 0.0:
-        raise ZeroFieldError("replay field is zero")
-    eff = s_fin[1] / s_fin[3]
-    if progress is not None:
-        progress(executed, errs[executed])
-    if gather:
-        parts = exch.gather([r.idx for r in ranks])
-        idx = np.concatenate([p.cpu().numpy() for p in parts], axis=0)
-    else:
-        idx = np.concatenate([r.idx.cpu().numpy() for r in ranks], axis=0)
-    for r in ranks:
-        close = getattr(r.ops, "close", None)
-        if close:
-            close()
-    holo = _native.expand_states(idx, states(cfg.slm.scheme)) if hasattr(idx, "dtype") else idx
+    sess = SlabSession(cfg, target, illumination, exchange=exchange, precision=precision, device=device,
+                       ops_factory=ops_factory)
+    try:
+        sums, executed, stopped = sess.run(progress=progress, cancel=cancel)
+        errs = sess.errors(sums, executed)
+        s_fin = sums[executed]
+        if s_fin[3] == 0.0:
+            raise ZeroFieldError("replay field is zero")
+        eff = s_fin[1] / s_fin[3]
+        if progress is not None:
+            progress(executed, errs[executed])
+        idx = sess.indices(gather)
+    finally:
+        sess.close()
+    holo = _native.expand_states(idx, states(cfg.slm.scheme))
     return holo, RunReport(
         error_trace=[(k, float(e)) for k, e in enumerate(errs)],
         final_error=float(errs[executed]),

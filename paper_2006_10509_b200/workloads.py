@@ -17,12 +17,16 @@ def natural_target(n, m=None, dx=0.0, dy=0.0):
     targets of config C5 use per-target offsets).
     """
     m = n if m is None else m
-    y, x = np.mgrid[0:m, 0:n].astype(np.float64)
-    sx, sy = n / 64.0, m / 64.0
-    img = 0.3 + 0.4 * np.exp(-(((x - (20 + 64 * dx) * sx) / sx) ** 2 + ((y - (24 + 64 * dy) * sy) / sy) ** 2) / 120.0)
-    img += 0.5 * np.exp(-(((x - (44 + 64 * dx) * sx) / sx) ** 2 + ((y - (40 + 64 * dy) * sy) / sy) ** 2) / 200.0)
-    img += 0.15 * np.sin(x / (6.0 * sx)) * np.cos(y / (9.0 * sy))
-    return np.clip(img, 0.0, 1.0).astype(np.complex128)
+    out = np.empty((m, n), np.complex128)
+    rows = max(1, (1 << 22) // n)   # same per-pixel formula, evaluated in row chunks (16384^2 planes)
+    for a in range(0, m, rows):
+        y, x = np.mgrid[a:min(m, a + rows), 0:n].astype(np.float64)
+        sx, sy = n / 64.0, m / 64.0
+        img = 0.3 + 0.4 * np.exp(-(((x - (20 + 64 * dx) * sx) / sx) ** 2 + ((y - (24 + 64 * dy) * sy) / sy) ** 2) / 120.0)
+        img += 0.5 * np.exp(-(((x - (44 + 64 * dx) * sx) / sx) ** 2 + ((y - (40 + 64 * dy) * sy) / sy) ** 2) / 200.0)
+        img += 0.15 * np.sin(x / (6.0 * sx)) * np.cos(y / (9.0 * sy))
+        out[a:a + rows] = np.clip(img, 0.0, 1.0)
+    return out
 
 
 def batched_target(n, target_id):
