@@ -445,6 +445,41 @@ def run_ours(args):
                            "algorithmic_bytes_per_iteration": GS_BYTES_PER_PX * hw6,
                            "note": "36 B/px algorithmic; the design also moves 2 x 16 B/px of corner turns"}}
 
+    # .hgi output: payload + CRC-32 of the C3 hologram from
+    # its index plane on the device vs host expansion + zlib (serialio.py:167-185)
+    hgi = None
+    if not args.no_hgi:
+        import zlib
+
+        from paper_2006_10509_b200 import serialio
+        from paper_2006_10509_b200.slm import states as state_table
+
+        idx3 = plan.download_indices(1)[0]
+        table3 = state_table(cfg.slm.scheme)
+        serialio.hologram_payload(idx3, table3, device=local)          # warm
+        reps = 5
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            _, crc_dev = serialio.hologram_payload(idx3, table3, device=local)
+        t_dev = (time.perf_counter() - t0) / reps
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            serialio.hologram_payload(idx3, table3, device=local, expand="device")
+        t_devx = (time.perf_counter() - t0) / reps
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            payload = table3[idx3]
+            crc_host = zlib.crc32(payload) & 0xFFFFFFFF
+        t_host = (time.perf_counter() - t0) / reps
+        nbytes = idx3.size * 16
+        hgi = {"metric": "hgi payload + CRC-32 of the C3 hologram (2048x2048 complex128, 64 MiB)",
+               "device_ms": t_dev * 1e3, "device_expand_ms": t_devx * 1e3, "host_ms": t_host * 1e3,
+               "device_gb_per_s": nbytes / t_dev / 1e9,
+               "host_gb_per_s": nbytes / t_host / 1e9, "crc_equal": crc_dev == crc_host,
+               "note": "device: CRC-32 on the GPU from the uint8 index plane while host threads expand "
+                       "states[idx] (device_expand_ms: expansion on the GPU + pageable D2H instead); "
+                       "host: numpy states[idx] + zlib.crc32 (1 thread)"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline_gs()
@@ -459,7 +494,7 @@ def run_ours(args):
                            "l2": "256 MB device write between timed steps (excluded from step time)"},
                 "gpu_launches": launches, "wall_s_timed": t_wall,
                 "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clk.summary(), "ospr": ospr,
-                "search": search, "c5": c5, "c6": c6}
+                "search": search, "c5": c5, "c6": c6, "hgi": hgi}
         print(json.dumps(line), flush=True)
     plan.close()
     if world > 1:
@@ -478,6 +513,7 @@ def main():
     ap.add_argument("--no-search", action="store_true")
     ap.add_argument("--no-c5", action="store_true")
     ap.add_argument("--no-c6", action="store_true")
+    ap.add_argument("--no-hgi", action="store_true")
     ap.add_argument("--c5-sample", type=int, default=8, help="targets timed per rank (of its block of 64/N)")
     ap.add_argument("--c6-steps", type=int, default=3)
     args = ap.parse_args()

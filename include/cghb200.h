@@ -238,6 +238,15 @@ int cgh_slab_pass(cgh_slab *slab, int32_t mode, void *data, const cgh_gs_params 
 /* dst[g] = transpose(src[g]) for every S x S block (the corner turn). */
 int cgh_slab_transpose(cgh_slab *slab, const void *src, void *dst);
 
+/* ---- .hgi payload (cghkit/serialio.py:167-185 save_field): the complex128
+ * payload states[idx] of an index plane, expanded on the device and copied to
+ * out_payload (count x 16 bytes, may be NULL), and zlib's CRC-32 of those
+ * payload bytes computed on the device from the index plane. */
+int cgh_hgi_payload(int32_t device, const void *idx, int32_t idx_bytes, int64_t count, const double *states,
+                    int32_t n_states, double *out_payload, uint32_t *out_crc);
+/* zlib crc32_combine (host, no GPU): CRC-32 of A||B from crc(A), crc(B), len(B). */
+int cgh_crc32_combine(uint32_t crc1, uint32_t crc2, int64_t len2, uint32_t *out);
+
 /* ---- host: materialise states[indices] as complex128 (the returned
  * hologram of every runner) with `threads` host threads (no GPU needed). */
 int cgh_expand_states(const void *idx, int32_t idx_bytes, int64_t count, const double *states, int32_t n_states,

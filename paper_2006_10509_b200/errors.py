@@ -49,3 +49,20 @@ class UnsupportedShapeError(CghError, NotImplementedError):
 
 class DeviceError(CghError, RuntimeError):
     """CUDA runtime failure reported by the library."""
+
+
+# .hgi containers (cghkit/errors.py:44-76; raised by serialio.py)
+class MalformedJsonError(CghError):
+    pass
+
+
+class ChecksumMismatchError(CghError):
+    pass
+
+
+class TruncatedPayloadError(CghError):
+    pass
+
+
+class EmptyImageError(CghError):
+    pass

@@ -1,0 +1,190 @@
+"""``.hgi`` field containers (cghkit/serialio.py:133-238), with the payload of
+generated holograms produced on the GPU.
+
+Container (identical bytes to the reference's ``save_field``): magic
+``HGI1``, a 4-byte little-endian header length, the UTF-8 JSON header
+``{width, height, checksum, metadata}``, then the row-major payload of
+little-endian (re, im) float64 pairs. ``checksum`` is zlib's CRC-32 of the
+payload bytes.
+
+``save_hologram`` writes a generator's output from its index plane: the
+CRC-32 of the 16 B/px complex128 payload is computed on the device from the
+1 B/px index plane (``cgh_hgi_payload``) while host threads expand
+``states[idx]``, so the payload is never checksummed in one host thread nor
+copied back from the device (C3 hologram: 2.2 ms vs 36 ms for numpy +
+zlib, ``bench.py`` key ``hgi``).
+``save_field``/``load_field``/``inspect_field`` keep the reference behaviour
+for arbitrary fields (host zlib, as the reference does).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import json
+import struct
+import zlib
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native
+from .errors import ChecksumMismatchError, EmptyImageError, MalformedJsonError, TruncatedPayloadError
+from .runtime import current_device
+
+HGI_MAGIC = b"HGI1"
+HGI_EXTENSION = ".hgi"
+_PAYLOAD_DTYPE = np.dtype("<c16")
+
+
+@dataclass
+class Metadata:
+    """Traceability record attached to every generated field (serialio.py:133-141)."""
+
+    parameters: list
+    seed: int
+    app_version: str
+    timestamp: str
+    algorithm: str
+    error_final: float
+    iterations: int
+
+
+def _metadata_to_json(meta: Metadata) -> dict:
+    return {
+        "parameters": [[path, value] for path, value in meta.parameters],
+        "seed": meta.seed,
+        "appVersion": meta.app_version,
+        "timestamp": meta.timestamp,
+        "algorithm": meta.algorithm,
+        "errorFinal": meta.error_final,
+        "iterations": meta.iterations,
+    }
+
+
+def _metadata_from_json(obj: dict) -> Metadata:
+    return Metadata(
+        parameters=[(path, value) for path, value in obj["parameters"]],
+        seed=int(obj["seed"]),
+        app_version=obj["appVersion"],
+        timestamp=obj["timestamp"],
+        algorithm=obj["algorithm"],
+        error_final=float(obj["errorFinal"]),
+        iterations=int(obj["iterations"]),
+    )
+
+
+def _write(path, width, height, checksum, meta, payload):
+    header = {"width": width, "height": height, "checksum": int(checksum) & 0xFFFFFFFF,
+              "metadata": _metadata_to_json(meta)}
+    header_bytes = json.dumps(header).encode("utf-8")
+    with open(path, "wb") as fh:
+        fh.write(HGI_MAGIC)
+        fh.write(struct.pack("<I", len(header_bytes)))
+        fh.write(header_bytes)
+        fh.write(memoryview(payload).cast("B"))
+
+
+def save_field(field, meta: Metadata, path) -> None:
+    """Write one complex field plus metadata (serialio.py:167-185)."""
+    field = np.asarray(field, dtype=np.complex128)
+    if field.ndim != 2 or field.size == 0:
+        raise EmptyImageError("field must be a non-empty 2D array")
+    height, width = field.shape
+    payload = np.ascontiguousarray(field).astype(_PAYLOAD_DTYPE, copy=False)
+    _write(path, width, height, zlib.crc32(payload) & 0xFFFFFFFF, meta, payload)
+
+
+def hologram_payload(indices, states, device=None, expand="host"):
+    """(complex128 payload states[indices], zlib CRC-32 of its bytes).
+
+    The CRC is always computed on the device from the 1 B/px index plane
+    (``cgh_hgi_payload``). The payload is expanded either by the host threads
+    of ``cgh_expand_states`` while the device checksums (``expand="host"``,
+    default: no 16 B/px device-to-host copy), or on the device and copied back
+    (``expand="device"``)."""
+    import threading
+
+    idx = np.ascontiguousarray(indices)
+    if idx.dtype not in (np.uint8, np.int32):
+        idx = np.ascontiguousarray(idx, dtype=np.int32)
+    table = np.ascontiguousarray(states, dtype=np.complex128)
+    lib = _native.library()
+    _native.require_device()
+    crc = ctypes.c_uint32(0)
+    dev = current_device() if device is None else device
+    status = []
+
+    def checksum(out_ptr):
+        status.append(lib.cgh_hgi_payload(dev, _native.ptr(idx), idx.dtype.itemsize, idx.size, _native.ptr(table),
+                                          len(table), out_ptr, ctypes.byref(crc)))
+
+    if expand == "device":
+        out = np.empty(idx.shape, dtype=np.complex128)
+        checksum(_native.ptr(out))
+    else:
+        worker = threading.Thread(target=checksum, args=(None,))
+        worker.start()                                   # the C call releases the GIL
+        out = _native.expand_states(idx, table)
+        worker.join()
+    _native.check(status[0])
+    return out, int(crc.value)
+
+
+def save_hologram(indices, states, meta: Metadata, path, device=None):
+    """Write the hologram ``states[indices]`` as an ``.hgi`` container (bytes
+    identical to ``save_field(states[indices], meta, path)``); returns the
+    complex128 hologram."""
+    idx = np.asarray(indices)
+    if idx.ndim != 2 or idx.size == 0:
+        raise EmptyImageError("field must be a non-empty 2D array")
+    holo, crc = hologram_payload(idx, states, device)
+    height, width = idx.shape
+    _write(path, width, height, crc, meta, holo)
+    return holo
+
+
+def _read_container(path):
+    with open(path, "rb") as fh:
+        blob = fh.read()
+    if len(blob) < 8 or blob[:4] != HGI_MAGIC:
+        raise MalformedJsonError(f"{path}: not an .hgi container")
+    header_len = struct.unpack("<I", blob[4:8])[0]
+    header_bytes = blob[8:8 + header_len]
+    if len(header_bytes) < header_len:
+        raise TruncatedPayloadError(f"{path}: header truncated")
+    try:
+        header = json.loads(header_bytes.decode("utf-8"))
+    except (UnicodeDecodeError, json.JSONDecodeError) as err:
+        raise MalformedJsonError(f"{path}: bad header ({err})") from None
+    return header, blob[8 + header_len:]
+
+
+def load_field(path):
+    """Read a container, verifying length and checksum (serialio.py:204-222)."""
+    header, payload = _read_container(path)
+    width, height = header["width"], header["height"]
+    expected = width * height * _PAYLOAD_DTYPE.itemsize
+    if len(payload) < expected:
+        raise TruncatedPayloadError(f"{path}: payload {len(payload)} bytes, expected {expected}")
+    if len(payload) > expected:
+        raise MalformedJsonError(f"{path}: trailing bytes after payload")
+    if zlib.crc32(payload) & 0xFFFFFFFF != header["checksum"]:
+        raise ChecksumMismatchError(f"{path}: payload checksum mismatch")
+    field = np.frombuffer(payload, dtype=_PAYLOAD_DTYPE).reshape(height, width)
+    return field.astype(np.complex128), _metadata_from_json(header["metadata"])
+
+
+def inspect_field(path):
+    """(header, metadata, checksum_ok) without raising on payload corruption."""
+    header, payload = _read_container(path)
+    expected = header["width"] * header["height"] * _PAYLOAD_DTYPE.itemsize
+    ok = len(payload) == expected and (zlib.crc32(payload) & 0xFFFFFFFF) == header["checksum"]
+    return header, _metadata_from_json(header["metadata"]), ok
+
+
+def crc32_combine(crc1, crc2, len2):
+    """zlib's crc32_combine through the library (host arithmetic, no GPU)."""
+    out = ctypes.c_uint32(0)
+    _native.check(_native.library().cgh_crc32_combine(ctypes.c_uint32(crc1), ctypes.c_uint32(crc2), int(len2),
+                                                      ctypes.byref(out)))
+    return int(out.value)
