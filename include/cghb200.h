@@ -247,6 +247,12 @@ int cgh_hgi_payload(int32_t device, const void *idx, int32_t idx_bytes, int64_t 
 /* zlib crc32_combine (host, no GPU): CRC-32 of A||B from crc(A), crc(B), len(B). */
 int cgh_crc32_combine(uint32_t crc1, uint32_t crc2, int64_t len2, uint32_t *out);
 
+/* ---- propagation.py:205-218 delta_replay_update on the device: in-place
+ * rank-1 update of an uncentred replay (h x w complex128, host memory) for a
+ * change `delta` of hologram pixel (m, n). */
+int cgh_delta_replay_update(int32_t device, double *replay, int32_t h, int32_t w, int32_t m, int32_t n,
+                            double delta_re, double delta_im);
+
 /* ---- host: materialise states[indices] as complex128 (the returned
  * hologram of every runner) with `threads` host threads (no GPU needed). */
 int cgh_expand_states(const void *idx, int32_t idx_bytes, int64_t count, const double *states, int32_t n_states,

@@ -217,3 +217,50 @@ int cgh_hgi_payload(int32_t device, const void* idx, int32_t idx_bytes, int64_t 
 }
 
 }  // extern "C"
+
+// ---- full-plane rank-1 replay update (cghkit/propagation.py:205-218,
+// SURVEY.md §8(f) #4): replay[u][v] += delta / sqrt(HW) * w_H^(m u) * w_W^(n v),
+// with the exponents reduced mod H / W into long-double-built 1-D tables.
+namespace cgh {
+__global__ void delta_update_kernel(double2* __restrict__ R, int H, int W, int m, int n, double2 d,
+                                    const double2* __restrict__ rt, const double2* __restrict__ ct) {
+    const long long total = (long long)H * W;
+    for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < total; p += (long long)gridDim.x * blockDim.x) {
+        const int u = int(p / W), v = int(p - (long long)u * W);
+        const double2 a = rt[(long long)m * u % H], b = ct[(long long)n * v % W];
+        const double2 w = make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+        R[p].x += d.x * w.x - d.y * w.y;
+        R[p].y += d.x * w.y + d.y * w.x;
+    }
+}
+}  // namespace cgh
+
+extern "C" int cgh_delta_replay_update(int32_t device, double* replay, int32_t h, int32_t w, int32_t m, int32_t n,
+                                       double delta_re, double delta_im) {
+    if (!replay || h < 1 || w < 1) return fail(CGH_ERR_VALUE, "bad arguments");
+    if (m < 0 || m >= h || n < 0 || n >= w) return fail(CGH_ERR_VALUE, "pixel (%d, %d) outside %dx%d", m, n, h, w);
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(CGH_ERR_NO_DEVICE, "no CUDA device");
+    if (device < 0 || device >= ndev) return fail(CGH_ERR_VALUE, "device %d out of range", device);
+    CGH_CUDA(cudaSetDevice(device));
+    std::vector<double> rt, ct;
+    twiddle_table(h, rt);
+    twiddle_table(w, ct);
+    const size_t n_el = size_t(h) * w;
+    double2 *d_r = nullptr, *d_rt = nullptr, *d_ct = nullptr;
+    CGH_CUDA(cudaMalloc(&d_r, n_el * 16));
+    CGH_CUDA(cudaMalloc(&d_rt, size_t(h) * 16));
+    CGH_CUDA(cudaMalloc(&d_ct, size_t(w) * 16));
+    cudaMemcpy(d_r, replay, n_el * 16, cudaMemcpyHostToDevice);
+    cudaMemcpy(d_rt, rt.data(), size_t(h) * 16, cudaMemcpyHostToDevice);
+    cudaMemcpy(d_ct, ct.data(), size_t(w) * 16, cudaMemcpyHostToDevice);
+    const double s = 1.0 / std::sqrt(double(h) * double(w));
+    delta_update_kernel<<<grid_for((long)n_el), 256>>>(d_r, h, w, m, n, make_double2(delta_re * s, delta_im * s), d_rt, d_ct);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpy(replay, d_r, n_el * 16, cudaMemcpyDeviceToHost);
+    cudaFree(d_r);
+    cudaFree(d_rt);
+    cudaFree(d_ct);
+    if (e != cudaSuccess) return fail(CGH_ERR_CUDA, "delta replay update: %s", cudaGetErrorString(e));
+    return CGH_OK;
+}
