@@ -201,7 +201,11 @@ def run_ours(args):
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        import datetime
+
+        # finite watchdog timeout: a rank that fails inside a collective leg
+        # must not leave the others blocked for the default 10 minutes
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local), timeout=datetime.timedelta(minutes=3))
 
     def barrier():
         if world > 1:
@@ -369,6 +373,7 @@ def run_ours(args):
     # rank (multi.shard), a bounded sample of each rank's block timed
     c5 = None
     if not args.no_c5:
+      try:
         from paper_2006_10509_b200.multi import shard
         from paper_2006_10509_b200.workloads import batched_target
 
@@ -409,11 +414,14 @@ def run_ours(args):
                            "frac": GS_BYTES_PER_PX * hw5 / (it_ms / 1000.0) / 1e9 / peak,
                            "algorithmic_bytes_per_iteration": GS_BYTES_PER_PX * hw5, "ms_per_iteration": it_ms}}
         c5plan.close()
+      except Exception as exc:  # noqa: BLE001 - reported in the JSON line, not fatal for the headline
+        c5 = {"error": f"{type(exc).__name__}: {exc}"}
 
     # C6: one 16384^2 GS plane over all ranks (row slabs, block-transpose corner
     # turns, NCCL all_to_all_single between passes when N > 1)
     c6 = None
     if not args.no_c6:
+      try:
         from paper_2006_10509_b200 import slab as SL
 
         c6cfg = make_cfg(1, n=C6_N, kind="fourier", iterations=C6_ITERS)
@@ -444,6 +452,8 @@ def run_ours(args):
                            "frac": GS_BYTES_PER_PX * hw6 / (ms6 / 1000.0) / 1e9 / world / peak,
                            "algorithmic_bytes_per_iteration": GS_BYTES_PER_PX * hw6,
                            "note": "36 B/px algorithmic; the design also moves 2 x 16 B/px of corner turns"}}
+      except Exception as exc:  # noqa: BLE001
+        c6 = {"error": f"{type(exc).__name__}: {exc}"}
 
     # .hgi output: payload + CRC-32 of the C3 hologram from
     # its index plane on the device vs host expansion + zlib (serialio.py:167-185)
