@@ -157,11 +157,12 @@ def run_reference(args):
     except Exception:  # noqa: BLE001
         cores = os.cpu_count() or 1
     m = 4
-    target = natural_target(N_PX)
+    n_ref = int(os.environ.get("CGHB200_BENCH_REF_N", N_PX))   # tests shrink the plane
+    target = natural_target(n_ref)
 
     def one(seed):
         stamps = []
-        cgh_oracle.gs(make_cfg(seed, iterations=m), target,
+        cgh_oracle.gs(make_cfg(seed, n=n_ref, iterations=m), target,
                       progress=lambda k, e: stamps.append((k, time.perf_counter())))
         loop = [s for s in stamps if s[0] < m]
         return loop[-1][0] - loop[0][0], loop[0][1], loop[-1][1]
@@ -174,7 +175,7 @@ def run_reference(args):
 
     with ThreadPoolExecutor(max_workers=cores) as pool:
         for w in range(args.warmup):
-            step(pool, -1 - w)
+            step(pool, args.steps + w)     # warm-up replicas use seeds after the timed ones
         tot_i, tot_t = 0, 0.0
         for s in range(args.steps):
             i, t = step(pool, s)
