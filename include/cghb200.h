@@ -237,6 +237,11 @@ int cgh_slab_pass(cgh_slab *slab, int32_t mode, void *data, const cgh_gs_params 
                   void *idx_out, double *sums);
 /* dst[g] = transpose(src[g]) for every S x S block (the corner turn). */
 int cgh_slab_transpose(cgh_slab *slab, const void *src, void *dst);
+/* Corner turn fused with the exchange: transpose(src[g]) is stored directly
+ * to dst_blocks[g] (G device pointers, e.g. rank g's receive buffer at chunk
+ * [this rank] through NVLink peer mappings). The caller orders the peers'
+ * next reads after it with a device barrier (one per turn). */
+int cgh_slab_turn(cgh_slab *slab, const void *src, void *const *dst_blocks);
 
 /* ---- .hgi payload (cghkit/serialio.py:167-185 save_field): the complex128
  * payload states[idx] of an index plane, expanded on the device and copied to

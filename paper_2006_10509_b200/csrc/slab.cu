@@ -271,6 +271,29 @@ int cgh_slab_pass(cgh_slab* slab, int32_t mode, void* data, const cgh_gs_params*
                                   : slab_pass<float>(slab, mode, data, gp, quantize, idx_out, sums);
 }
 
+int cgh_slab_turn(cgh_slab* slab, const void* src, void* const* dst_blocks) {
+    if (!slab || !src || !dst_blocks) return fail(CGH_ERR_VALUE, "null slab or buffer");
+    if (slab->G > kMaxTurnBlocks) return fail(CGH_ERR_UNSUPPORTED, "at most %d ranks", kMaxTurnBlocks);
+    CGH_CUDA(cudaSetDevice(slab->dev));
+    const int S = slab->R;
+    dim3 grid((S + 31) / 32, (S + 31) / 32, slab->G), block(32, 8);
+    for (int g = 0; g < slab->G; ++g) {
+        if (!dst_blocks[g]) return fail(CGH_ERR_VALUE, "null destination block %d", g);
+        if (dst_blocks[g] == src) return fail(CGH_ERR_VALUE, "turn destination aliases the source");
+    }
+    if (slab->prec == CGH_FP64) {
+        TurnTargets<double> t;
+        for (int g = 0; g < slab->G; ++g) t.p[g] = static_cast<cx<double>*>(dst_blocks[g]);
+        slab_turn_kernel<double><<<grid, block, 0, slab->st>>>(static_cast<const cx<double>*>(src), t, S);
+    } else {
+        TurnTargets<float> t;
+        for (int g = 0; g < slab->G; ++g) t.p[g] = static_cast<cx<float>*>(dst_blocks[g]);
+        slab_turn_kernel<float><<<grid, block, 0, slab->st>>>(static_cast<const cx<float>*>(src), t, S);
+    }
+    CGH_CUDA(cudaGetLastError());
+    return CGH_OK;
+}
+
 int cgh_slab_transpose(cgh_slab* slab, const void* src, void* dst) {
     if (!slab || !src || !dst) return fail(CGH_ERR_VALUE, "null slab or buffer");
     if (src == dst) return fail(CGH_ERR_VALUE, "transpose needs distinct buffers");

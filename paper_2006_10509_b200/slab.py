@@ -133,13 +133,27 @@ def from_segments(seg):
 # ------------------------------------------------------------------ exchanges
 
 
+def _fused_turn_targets(ranks_dst_ptrs, my_rank, block_bytes):
+    """Destinations of this rank's G blocks for the fused corner turn: block g
+    goes to rank g's receive buffer at chunk [my_rank]."""
+    return [base + my_rank * block_bytes for base in ranks_dst_ptrs]
+
+
 class LocalExchange:
     """G = 1: the corner turn is a plain transpose, no collective."""
 
     world = 1
 
-    def all_to_all(self, sends, recvs):
-        raise AssertionError("no exchange at G = 1")
+    def alloc(self, ops, shape):
+        return ops.empty(shape), ops.empty(shape)
+
+    def turn(self, ranks, src, dst):
+        r = ranks[0]
+        s, d = getattr(r, src), getattr(r, dst)
+        if hasattr(r.ops, "turn"):
+            r.ops.turn(s, [d.data_ptr()])
+        else:
+            r.ops.transpose(s, d)
 
     def all_reduce(self, tensors):
         return tensors
@@ -149,7 +163,10 @@ class LocalExchange:
 
 
 class TorchExchange:
-    """One rank of a torch.distributed group (NCCL on GPUs, gloo on CPU)."""
+    """One rank of a torch.distributed group (NCCL on GPUs, gloo on CPU): the
+    corner turn is block transposes into a send buffer + all_to_all_single."""
+
+    needs_send_buffer = True
 
     def __init__(self, group=None):
         import torch.distributed as dist
@@ -159,12 +176,16 @@ class TorchExchange:
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
 
-    def all_to_all(self, sends, recvs):
+    def alloc(self, ops, shape):
+        return ops.empty(shape), ops.empty(shape)
+
+    def turn(self, ranks, src, dst):
         import torch
 
-        (send,), (recv,) = sends, recvs
+        (r,) = ranks
+        r.ops.transpose(getattr(r, src), r.B)
         # complex slabs travel as (re, im) pairs: chunk g (R*R elements) -> rank g
-        self.dist.all_to_all_single(torch.view_as_real(recv), torch.view_as_real(send), group=self.group)
+        self.dist.all_to_all_single(torch.view_as_real(getattr(r, dst)), torch.view_as_real(r.B), group=self.group)
 
     def all_reduce(self, tensors):
         (t,) = tensors
@@ -180,17 +201,72 @@ class TorchExchange:
         return parts
 
 
+class SymmetricExchange(TorchExchange):
+    """One rank of a CUDA group with NVLink peer mappings (torch symmetric
+    memory): the slab buffers live in one symmetric allocation, and the corner
+    turn is ONE kernel per rank that transposes each block and stores it into
+    the owning peer's buffer (cgh_slab_turn), followed by a device barrier.
+    No NCCL on the data path."""
+
+    needs_send_buffer = False
+
+    def __init__(self, group=None):
+        super().__init__(group)
+        self.handle = None
+        self.peer_base = None
+        import torch.distributed._symmetric_memory as symm
+
+        g = self.group if self.group is not None else self.dist.group.WORLD
+        try:   # required before rendezvous on some torch versions, a no-op on others
+            symm.enable_symm_mem_for_group(g.group_name)
+        except Exception:  # noqa: BLE001
+            pass
+
+    def alloc(self, ops, shape):
+        import torch.distributed._symmetric_memory as symm
+
+        buf = symm.empty((2,) + tuple(shape), dtype=ops.cdtype, device=ops.device)
+        group = self.group if self.group is not None else self.dist.group.WORLD
+        self.handle = symm.rendezvous(buf, group)
+        self.peer_base = list(self.handle.buffer_ptrs)
+        self.half = buf[0].numel() * buf.element_size()      # byte offset of C inside the allocation
+        self.block_bytes = buf[0, 0].numel() * buf.element_size()
+        self.buf = buf
+        return buf[0], buf[1]
+
+    def turn(self, ranks, src, dst):
+        (r,) = ranks
+        off = 0 if dst == "A" else self.half
+        r.ops.turn(getattr(r, src), _fused_turn_targets([b + off for b in self.peer_base], self.rank, self.block_bytes))
+        self.handle.barrier(channel=0)
+
+
 class SimulatedExchange:
     """G virtual ranks in one process on one device (tests): phases run rank
-    after rank, the all-to-all is block copies, so no kernel waits on another."""
+    after rank and no kernel waits on another. With device ops the corner turn
+    is the same fused kernel as SymmetricExchange, storing into the other
+    virtual ranks' buffers (so its addressing is exercised here); otherwise
+    transposes + block copies."""
 
     def __init__(self, world):
         self.world = world
 
-    def all_to_all(self, sends, recvs):
-        for h, recv in enumerate(recvs):
-            for g, send in enumerate(sends):
-                recv[g].copy_(send[h])
+    def alloc(self, ops, shape):
+        return ops.empty(shape), ops.empty(shape)
+
+    def turn(self, ranks, src, dst):
+        if all(hasattr(r.ops, "turn") for r in ranks):
+            bases = [getattr(r, dst).data_ptr() for r in ranks]
+            for h, r in enumerate(ranks):
+                s = getattr(r, src)
+                r.ops.turn(s, _fused_turn_targets(bases, h, s[0].numel() * s.element_size()))
+            return
+        for r in ranks:
+            r.ops.transpose(getattr(r, src), r.B)
+        for h, r in enumerate(ranks):
+            recv = getattr(r, dst)
+            for g, q in enumerate(ranks):
+                recv[g].copy_(q.B[h])
 
     def all_reduce(self, tensors):
         total = tensors[0].clone()
@@ -256,6 +332,11 @@ class NativeOps:
         _native.check(self.lib.cgh_slab_transpose(self.handle, ctypes.c_void_p(src.data_ptr()),
                                                   ctypes.c_void_p(dst.data_ptr())))
 
+    def turn(self, src, dst_ptrs):
+        """Fused corner turn: transpose(src[g]) -> dst_ptrs[g] (device addresses)."""
+        arr = (ctypes.c_void_p * len(dst_ptrs))(*[ctypes.c_void_p(int(p)) for p in dst_ptrs])
+        _native.check(self.lib.cgh_slab_turn(self.handle, ctypes.c_void_p(src.data_ptr()), arr))
+
     def sync(self):
         self.torch.cuda.synchronize(self.device)
 
@@ -265,29 +346,24 @@ class NativeOps:
 
 class SlabRank:
     """Buffers and passes of one rank: A (hologram slab), C (replay slab),
-    B (send buffer), the local index plane and the per-iteration sums."""
+    B (send buffer, NCCL exchange only), the local index plane and the
+    per-iteration sums."""
 
-    def __init__(self, ops, world, n, iters):
+    def __init__(self, ops, world, n, iters, exch):
         self.ops = ops
         self.G, self.N, self.R = world, n, n // world
         shape = (world, self.R, self.R)
-        self.A = ops.empty(shape)
-        self.C = ops.empty(shape)
-        self.B = ops.empty(shape) if world > 1 else None
+        self.A, self.C = exch.alloc(ops, shape)
+        need_b = world > 1 and (getattr(exch, "needs_send_buffer", False) or not hasattr(ops, "turn"))
+        self.B = ops.empty(shape) if need_b else None
         self.idx = ops.empty((self.R, n), "idx")
         self.sums = ops.empty((iters + 1, 4), "f64")
         self.sums.zero_()
 
 
 def _turn(ranks, exch, src, dst):
-    """Corner turn src -> dst on every rank (block transposes + all-to-all)."""
-    if exch.world == 1:
-        r = ranks[0]
-        r.ops.transpose(getattr(r, src), getattr(r, dst))
-        return
-    for r in ranks:
-        r.ops.transpose(getattr(r, src), r.B)
-    exch.all_to_all([r.B for r in ranks], [getattr(r, dst) for r in ranks])
+    """Corner turn src -> dst on every rank (see the exchange classes)."""
+    exch.turn(ranks, src, dst)
 
 
 def _validate(stats, init_code, iters):
@@ -411,7 +487,7 @@ class SlabSession:
             def ops_factory(rk):
                 return NativeOps(cfg, n, world, rk, prec, dev, stream)
 
-        self.ranks = [SlabRank(ops_factory(rk), world, n, self.iters) for rk in rank_ids]
+        self.ranks = [SlabRank(ops_factory(rk), world, n, self.iters, self.exch) for rk in rank_ids]
         for r, loc in zip(self.ranks, self.local):
             r.ops.set_local(loc["tgt"], loc["beam"])
 

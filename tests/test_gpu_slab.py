@@ -164,3 +164,48 @@ def test_slab_16384_single_rank():
     assert 0.0 < rep.efficiency <= 1.0
     # the hologram takes only state values
     assert np.all(np.isin(holo[::257, ::263], A.states(cfg.slm.scheme)))
+
+
+def _symm_worker(proc, out_path):
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        cfg = _cfg(256, "fresnel", 8, True, 0.2, False, "random-phase", iters=5)
+        target = natural_target(256)
+        with precision("fp64"):
+            holo, rep = SL.run_gs_slab(cfg, target, exchange=SL.SymmetricExchange())
+        np.save(out_path, holo)
+        with open(out_path + ".trace", "w") as f:
+            f.write(repr([e for _, e in rep.error_trace]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_symmetric_memory_exchange_single_rank(tmp_path):
+    """The NVLink peer-memory exchange (torch symmetric memory: one allocation
+    for both slabs, rendezvous, peer pointers, fused turn kernel, device
+    barrier) on a one-rank NCCL group equals the plain G = 1 run."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    import os
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    out = str(tmp_path / "holo.npy")
+    mp.spawn(_symm_worker, args=(out,), nprocs=1, join=True)
+    cfg = _cfg(256, "fresnel", 8, True, 0.2, False, "random-phase", iters=5)
+    holo, rep = _run(cfg, natural_target(256), None, 1, "fp64")
+    assert np.array_equal(np.load(out), holo)
+    tr = eval(open(out + ".trace").read())
+    assert rel(tr, [e for _, e in rep.error_trace]) < 1e-14
