@@ -193,6 +193,23 @@ int cgh_plan_sa(cgh_plan *plan, const cgh_sa_params *sp, int64_t *trace_k, doubl
 int cgh_plan_dbs(cgh_plan *plan, const cgh_dbs_params *dp, int64_t *trace_k, double *trace_v, int64_t trace_cap,
                  cgh_report *rep, const cgh_callbacks *cb);     /* plan must be CGH_FP64 */
 int cgh_plan_download_idx(cgh_plan *plan, void *out_idx, int64_t frames);
+/* OSPR sharded over subframes: this plan's contiguous
+ * part [frame0, frame0 + op->subframes) (1..64 frames, op->frame_rng = their
+ * streams) of an nframes_total-subframe run. Phase 1 generates the part
+ * (index planes final) and leaves its own |R|^2 total in the plan's intensity
+ * plane; the caller sets the plane to the lower parts' totals
+ * (cgh_plan_set_intensity) and phase 2 re-accumulates with the global frame
+ * numbers: trace = the reference's cumulative errors of these frames, and the
+ * efficiency when the part ends the run. */
+int cgh_plan_ospr_part(cgh_plan *plan, const cgh_ospr_params *op, int32_t frame0, int32_t nframes_total,
+                       int32_t phase, int64_t *trace_k, double *trace_v, int64_t trace_cap, cgh_report *rep);
+/* intensity plane := sum of `count` device planes (H*W of the plan's real
+ * type; peer pointers allowed), fixed order 0, 1, ...; count 0 zeroes it. */
+int cgh_plan_set_intensity(cgh_plan *plan, const void *const *planes, int32_t count);
+/* copy the intensity plane (H*W reals) to device address dst */
+int cgh_plan_copy_intensity(cgh_plan *plan, void *dst);
+/* device address / bytes of the plan's intensity plane */
+int cgh_plan_intensity(cgh_plan *plan, void **out_ptr, int64_t *out_bytes);
 void *cgh_plan_stream(cgh_plan *plan);          /* cudaStream_t of the plan */
 /* Per-pass CUDA-event timing: returns the accumulated ms / launch counts per
  * pass id since the last call (ids: row modes 0-7, column modes 8-15, search

@@ -39,7 +39,8 @@ EXPORTS = (
     "cgh_delta_error", "cgh_commit_update", "cgh_best_delta",
     "cgh_permutation", "cgh_random_doubles", "cgh_expand_states",
     "cgh_slab_create", "cgh_slab_destroy", "cgh_slab_set_local", "cgh_slab_pass", "cgh_slab_transpose",
-    "cgh_slab_turn",
+    "cgh_slab_turn", "cgh_plan_ospr_part", "cgh_plan_set_intensity", "cgh_plan_intensity",
+    "cgh_plan_copy_intensity",
     "cgh_hgi_payload", "cgh_crc32_combine", "cgh_delta_replay_update",
 )
 
@@ -164,6 +165,10 @@ def _declare(lib):
         "cgh_slab_pass": ([P, i32, P, pP(GsParams), i32, P, P], ctypes.c_int),
         "cgh_slab_transpose": ([P, P, P], ctypes.c_int),
         "cgh_slab_turn": ([P, P, P], ctypes.c_int),
+        "cgh_plan_ospr_part": ([P, pP(OsprParams), i32, i32, i32, P, P, i64, pP(Report)], ctypes.c_int),
+        "cgh_plan_set_intensity": ([P, P, i32], ctypes.c_int),
+        "cgh_plan_intensity": ([P, pP(P), pP(i64)], ctypes.c_int),
+        "cgh_plan_copy_intensity": ([P, P], ctypes.c_int),
         "cgh_hgi_payload": ([i32, P, i32, i64, P, i32, P, pP(ctypes.c_uint32)], ctypes.c_int),
         "cgh_crc32_combine": ([ctypes.c_uint32, ctypes.c_uint32, i64, pP(ctypes.c_uint32)], ctypes.c_int),
         "cgh_delta_replay_update": ([i32, P, i32, i32, i32, i32, f64, f64], ctypes.c_int),

@@ -633,6 +633,125 @@ static int ospr_exec(cgh_plan* P, const cgh_ospr_params* op, int64_t* tk, double
     return CGH_OK;
 }
 
+// ====================================================== sharded OSPR part
+// One rank's contiguous range [frame0, frame0 + m) of the S subframes of a
+// run_ospr sharded across GPUs. Phase 1 generates the
+// local subframes (K1, K2: index planes final) and accumulates their |R|^2
+// from a zero base into the plan's intensity plane. The caller then sets the
+// plane to the sum of the lower ranks' totals (cgh_plan_set_intensity) and
+// phase 2 re-runs only K3 over the resident subframes with the global frame
+// numbers, giving the reference's cumulative per-frame errors; the rank
+// holding frame S-1 also gets the efficiency.
+template <class T>
+static int ospr_part_exec(cgh_plan* P, const cgh_ospr_params* op, int frame0, int nframes_total, int phase,
+                          int64_t* tk, double* tv, int64_t cap, cgh_report* rep) {
+    if (!P->target_ready) return fail(CGH_ERR_VALUE, "target not set");
+    const int m = std::max(0, op->subframes);
+    if (m < 1 || m > 64) return fail(CGH_ERR_UNSUPPORTED, "a sharded OSPR part holds 1..64 subframes (got %d)", m);
+    if (frame0 < 0 || frame0 + m > nframes_total) return fail(CGH_ERR_VALUE, "frames [%d, %d) outside %d", frame0, frame0 + m, nframes_total);
+    if (phase != 1 && phase != 2) return fail(CGH_ERR_VALUE, "phase must be 1 or 2");
+    if (P->nf_all > 0) return fail(CGH_ERR_NONFINITE, "target contains NaN or Inf");
+    if (P->nf_beam > 0) return fail(CGH_ERR_NONFINITE, "illumination contains NaN or Inf");
+    if (P->count_in == 0) return fail(CGH_ERR_EMPTY_MASK, "metric mask has no true pixels");
+    if (P->denom == 0) return fail(CGH_ERR_ZERO_TARGET, "target is zero inside the mask");
+    const long n = long(P->H) * P->W;
+    const long launches0 = P->launches;
+    CGH_TRY(ensure(P, P->intensity, size_t(n) * sizeof(T)));
+    const int nb = std::max(row_grid_blocks<T>(P->W, P->H), col_grid_blocks<T>(P->H, P->W));
+    CGH_TRY(ensure(P, P->partials, size_t(nb) * (3 * 64 + 2) * sizeof(double)));
+    CGH_TRY(ensure_res(P, size_t(nframes_total + 2)));
+    if (phase == 1) {   // buffers before base_args() captures their addresses
+        if (!op->frame_rng) return fail(CGH_ERR_VALUE, "frame streams missing");
+        CGH_TRY(ensure(P, P->data, size_t(n) * sizeof(cx<T>) * m));
+        CGH_TRY(ensure(P, P->idx, size_t(n) * P->idx_bytes * m));
+        CGH_TRY(ensure(P, P->frame_rng, sizeof(Pcg64) * m));
+    } else if (P->data.cap < size_t(n) * sizeof(cx<T>) * m) {
+        return fail(CGH_ERR_VALUE, "phase 2 needs the frames of phase 1 on this plan");
+    }
+    PassArgs<T> a = base_args<T>(P);
+    a.intensity = static_cast<T*>(P->intensity.p);
+    a.red.out = P->res_d;
+    a.frames = m;
+    CGH_CUDA(cudaEventRecord(P->ev0, P->st));
+    if (phase == 1) {
+        std::vector<Pcg64> fr(m);
+        for (int i = 0; i < m; ++i) fr[i] = to_pcg(op->frame_rng[i]);
+        CGH_CUDA(cudaMemcpyAsync(P->frame_rng.p, fr.data(), sizeof(Pcg64) * m, cudaMemcpyHostToDevice, P->st));
+        CGH_CUDA(cudaStreamSynchronize(P->st));   // fr is a temporary
+        a.frame_rng = static_cast<const Pcg64*>(P->frame_rng.p);
+        // local numbering for the streams; errors of this phase are not used
+        a.frame0 = 0;
+        a.nframes_total = m;
+        bool fast = false;
+        if constexpr (sizeof(T) == 4) fast = fast_ospr_eligible(P);
+        if constexpr (sizeof(T) == 4) {
+            if (fast) CGH_TRY(fast_ospr_gen(P, a));
+            else CGH_TRY(run_row<T>(P, ROW_OSPR_GEN, a, m));
+        } else {
+            CGH_TRY(run_row<T>(P, ROW_OSPR_GEN, a, m));
+        }
+        PassArgs<T> b = a;
+        b.quantize = 1;
+        b.idx_out = P->idx.p;
+        bool fast_done = false;
+        if constexpr (sizeof(T) == 4) {
+            if (fast) {
+                CGH_TRY(fast_ospr_holo(P, b, m, m, static_cast<uint8_t*>(b.idx_out)));
+                fast_done = true;
+            }
+        }
+        if (!fast_done) CGH_TRY(run_col<T>(P, COL_HOLO, b, m));
+        P->idx_frames = m;
+    }
+    // K3: phase 1 from a zero base, phase 2 from the base the caller loaded
+    PassArgs<T> c = a;
+    c.frame0 = phase == 1 ? 0 : frame0;
+    c.nframes_total = phase == 1 ? m : nframes_total;
+    c.load_intensity = phase == 2 ? 1 : 0;
+    c.store_intensity = 1;
+    bool fast = false;
+    if constexpr (sizeof(T) == 4) fast = fast_ospr_eligible(P);
+    if constexpr (sizeof(T) == 4) {
+        if (fast) CGH_TRY(fast_ospr_acc(P, c));
+        else CGH_TRY(run_row<T>(P, ROW_OSPR_ACC, c, 1));
+    } else {
+        CGH_TRY(run_row<T>(P, ROW_OSPR_ACC, c, 1));
+    }
+    CGH_CUDA(cudaEventRecord(P->ev1, P->st));
+    CGH_CUDA(cudaEventSynchronize(P->ev1));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, P->ev0, P->ev1);
+    volatile const double* res = P->res_h;
+    const bool tail = phase == 2 && frame0 + m == nframes_total;
+    if (tk && tv) {
+        if (cap < m) return fail(CGH_ERR_VALUE, "trace capacity %lld < %d", (long long)cap, m);
+        for (int f = 0; f < m; ++f) {
+            tk[f] = (phase == 2 ? frame0 : 0) + f + 1;
+            tv[f] = res[(phase == 2 ? frame0 : 0) + f];
+        }
+    }
+    if (rep) {
+        rep->final_error = res[(phase == 2 ? frame0 : 0) + m - 1];
+        rep->efficiency = tail ? res[nframes_total] : std::nan("");
+        if (tail && std::isnan(rep->efficiency)) return fail(CGH_ERR_ZERO_FIELD, "replay field is zero");
+        rep->iterations_executed = m;
+        rep->termination = CGH_COMPLETED;
+        rep->trace_len = m;
+        rep->kernel_launches = P->launches - launches0;
+        rep->device_ms = ms;
+    }
+    return CGH_OK;
+}
+
+template <class T>
+__global__ void sum_planes_kernel(const T* const* __restrict__ planes, int count, long n, T* __restrict__ out) {
+    for (long p = (long)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (long)gridDim.x * blockDim.x) {
+        T s = T(0);
+        for (int i = 0; i < count; ++i) s += planes[i][p];   // fixed order: planes 0, 1, ...
+        out[p] = s;
+    }
+}
+
 // ============================================================== quantize
 __global__ void quantize_kernel(const double* __restrict__ v, long n, SchemeDev s, int32_t* __restrict__ out) {
     for (long i = long(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += long(gridDim.x) * blockDim.x)
@@ -760,6 +879,55 @@ int cgh_plan_ospr(cgh_plan* plan, const cgh_ospr_params* op, int64_t* trace_k, d
     CGH_CUDA(cudaSetDevice(plan->dev));
     return plan->prec == CGH_FP64 ? ospr_exec<double>(plan, op, trace_k, trace_v, trace_cap, rep, cb)
                                   : ospr_exec<float>(plan, op, trace_k, trace_v, trace_cap, rep, cb);
+}
+
+int cgh_plan_ospr_part(cgh_plan* plan, const cgh_ospr_params* op, int32_t frame0, int32_t nframes_total,
+                       int32_t phase, int64_t* trace_k, double* trace_v, int64_t trace_cap, cgh_report* rep) {
+    if (!plan || !op) return fail(CGH_ERR_VALUE, "null argument");
+    CGH_CUDA(cudaSetDevice(plan->dev));
+    return plan->prec == CGH_FP64
+               ? ospr_part_exec<double>(plan, op, frame0, nframes_total, phase, trace_k, trace_v, trace_cap, rep)
+               : ospr_part_exec<float>(plan, op, frame0, nframes_total, phase, trace_k, trace_v, trace_cap, rep);
+}
+
+int cgh_plan_set_intensity(cgh_plan* plan, const void* const* planes, int32_t count) {
+    if (!plan || count < 0 || (count > 0 && !planes)) return fail(CGH_ERR_VALUE, "bad arguments");
+    CGH_CUDA(cudaSetDevice(plan->dev));
+    const long n = long(plan->H) * plan->W;
+    const size_t es = plan->prec == CGH_FP64 ? 8 : 4;
+    CGH_TRY(ensure(plan, plan->intensity, size_t(n) * es));
+    void* d_ptrs = nullptr;
+    if (count > 0) {
+        CGH_CUDA(cudaMallocAsync(&d_ptrs, sizeof(void*) * count, plan->st));
+        CGH_CUDA(cudaMemcpyAsync(d_ptrs, planes, sizeof(void*) * count, cudaMemcpyHostToDevice, plan->st));
+    }
+    if (plan->prec == CGH_FP64)
+        sum_planes_kernel<double><<<grid_for(n), 256, 0, plan->st>>>(static_cast<const double* const*>(d_ptrs), count, n,
+                                                                     static_cast<double*>(plan->intensity.p));
+    else
+        sum_planes_kernel<float><<<grid_for(n), 256, 0, plan->st>>>(static_cast<const float* const*>(d_ptrs), count, n,
+                                                                    static_cast<float*>(plan->intensity.p));
+    plan->launches += 1;
+    CGH_CUDA(cudaGetLastError());
+    if (d_ptrs) CGH_CUDA(cudaFreeAsync(d_ptrs, plan->st));
+    CGH_CUDA(cudaStreamSynchronize(plan->st));   // `planes` is a host temporary of the caller
+    return CGH_OK;
+}
+
+int cgh_plan_copy_intensity(cgh_plan* plan, void* dst) {
+    if (!plan || !dst || !plan->intensity.p) return fail(CGH_ERR_VALUE, "no intensity plane");
+    CGH_CUDA(cudaSetDevice(plan->dev));
+    const size_t bytes = size_t(plan->H) * plan->W * (plan->prec == CGH_FP64 ? 8 : 4);
+    CGH_CUDA(cudaMemcpyAsync(dst, plan->intensity.p, bytes, cudaMemcpyDeviceToDevice, plan->st));
+    CGH_CUDA(cudaStreamSynchronize(plan->st));
+    return CGH_OK;
+}
+
+int cgh_plan_intensity(cgh_plan* plan, void** out_ptr, int64_t* out_bytes) {
+    if (!plan || !out_ptr) return fail(CGH_ERR_VALUE, "bad arguments");
+    *out_ptr = plan->intensity.p;
+    if (out_bytes) *out_bytes = int64_t(plan->intensity.cap);
+    return CGH_OK;
 }
 
 int cgh_plan_download_idx(cgh_plan* plan, void* out_idx, int64_t frames) {

@@ -6,7 +6,7 @@ with no data-path collective; only the per-job reports are gathered. SA/DBS
 runs are sequential per proposal, so several GPUs run replicas (independent
 seeds/targets) — "replicas only".
 
-Two front ends:
+Three front ends:
 
 * ``run_batch(jobs, devices)`` — one process driving several GPUs with one
   host thread per device (the C ABI releases the GIL), mirroring the
@@ -17,6 +17,12 @@ Two front ends:
   ``torch.distributed`` (torchrun); rank r runs the contiguous block
   ``shard(len(jobs), world, r)`` and the reports are gathered to every rank
   with ``all_gather_object`` (gloo on CPU for tests, NCCL on GPUs).
+* ``run_ospr_sharded(cfg, target, exchange=...)`` — ONE ``run_ospr`` with its
+  S subframes split into contiguous parts over the ranks:
+  each rank generates its part (index planes), publishes its |R|^2 total, and
+  re-accumulates from the sum of the lower ranks' totals (one exchange step:
+  read through peer pointers with symmetric memory, or NCCL all-gather) so the
+  cumulative per-frame errors equal the single-GPU run's.
 """
 
 from __future__ import annotations
@@ -119,3 +125,114 @@ def run_sharded(jobs, runner=None, group=None, device_index=None, keep_holograms
     gathered = [None] * world
     dist.all_gather_object(gathered, mine, group=group)
     return [r for part in gathered for r in part]
+
+
+def _ospr_plane_exchange(plans, exch, rank_ids, world):
+    """Phase-1 totals -> each rank's base = sum of the lower ranks' totals.
+
+    SimulatedExchange: the planes are the other virtual ranks' intensity
+    buffers (same device). SymmetricExchange: each rank copies its total into
+    a symmetric plane; after a device barrier the base kernel reads the lower
+    ranks' planes through NVLink peer pointers. Otherwise (NCCL/gloo): all-gather
+    into a (G, H, W) tensor and sum its first rank planes on the device."""
+    import torch
+
+    from .slab import SimulatedExchange, SymmetricExchange, TorchExchange
+
+    if not isinstance(exch, TorchExchange):   # LocalExchange / SimulatedExchange: all ranks in this process
+        # the base of rank r reads ranks 0..r-1 before any rank overwrites its
+        # own plane, so stage copies first
+        n_el = plans[0].shape[0] * plans[0].shape[1]
+        dt = torch.float64 if plans[0].pb.precision == 1 else torch.float32
+        dev = torch.device("cuda", plans[0].pb.device)
+        stage = []
+        for p in plans:
+            t = torch.empty(n_el, dtype=dt, device=dev)
+            p.copy_intensity(t.data_ptr())
+            stage.append(t)
+        for r, p in zip(rank_ids, plans):
+            p.set_intensity([stage[i].data_ptr() for i in range(r)])
+        return
+    (p,) = plans
+    rank = rank_ids[0]
+    n_el = p.shape[0] * p.shape[1]
+    dt = torch.float64 if p.pb.precision == 1 else torch.float32
+    dev = torch.device("cuda", p.pb.device)
+    if isinstance(exch, SymmetricExchange):
+        import torch.distributed._symmetric_memory as symm
+
+        plane = symm.empty(n_el, dtype=dt, device=dev)
+        group = exch.group if exch.group is not None else exch.dist.group.WORLD
+        h = symm.rendezvous(plane, group)
+        p.copy_intensity(plane.data_ptr())
+        h.barrier(channel=0)
+        p.set_intensity(list(h.buffer_ptrs)[:rank])
+        h.barrier(channel=0)                 # peers finished reading this rank's plane
+        return
+    mine = torch.empty(n_el, dtype=dt, device=dev)
+    p.copy_intensity(mine.data_ptr())
+    allp = torch.empty((world, n_el), dtype=dt, device=dev)
+    exch.dist.all_gather_into_tensor(allp, mine, group=exch.group)
+    p.set_intensity([allp[i].data_ptr() for i in range(rank)])
+
+
+def run_ospr_sharded(cfg, target, illumination=None, *, exchange=None, gather=True, precision=None, device=None):
+    """``run_ospr`` (algorithms.py:473-530) with the subframes sharded over
+    ranks. Returns (list of complex128 subframe holograms — all S when
+    ``gather``, else this rank's part —, RunReport) on every rank."""
+    import time
+
+    import numpy as np
+
+    from .algorithms import COMPLETED, RunReport, _check_inputs
+    from .plan import GenerationPlan
+    from .slab import LocalExchange, SimulatedExchange
+    from .slm import states
+
+    start = time.perf_counter()
+    target = np.asarray(target, dtype=np.complex128)
+    _check_inputs(cfg, target, illumination)
+    exch = exchange or LocalExchange()
+    world = exch.world
+    S = int(cfg.subframes)
+    streams = np.random.SeedSequence(cfg.seed).spawn(S)   # algorithms.py:487
+    rank_ids = list(range(world)) if isinstance(exch, SimulatedExchange) else [getattr(exch, "rank", 0)]
+    parts = [shard(S, world, r) for r in rank_ids]
+    plans = []
+    for r, (lo, hi) in zip(rank_ids, parts):
+        p = GenerationPlan(cfg, target.shape, precision=precision, device=device)
+        p.set_target(target, illumination)
+        if hi > lo:
+            p.ospr_part(streams[lo:hi], lo, S, 1)
+        else:
+            p.set_intensity([])
+        plans.append(p)
+    _ospr_plane_exchange(plans, exch, rank_ids, world)
+    local_trace, eff, idx_parts = [], None, []
+    for p, (lo, hi) in zip(plans, parts):
+        if hi > lo:
+            rep, tr = p.ospr_part(streams[lo:hi], lo, S, 2)
+            local_trace += tr
+            if hi == S:
+                eff = float(rep.efficiency)
+            idx_parts.append(p.download_indices(hi - lo))
+        else:
+            idx_parts.append(np.empty((0,) + target.shape, np.uint8))
+    for p in plans:
+        p.close()
+    if isinstance(exch, SimulatedExchange) or world == 1:
+        traces, effs, idxs = [local_trace], [eff], idx_parts
+    else:
+        import torch.distributed as dist
+
+        got = [None] * world
+        dist.all_gather_object(got, (local_trace, eff, idx_parts[0] if gather else None), group=exch.group)
+        traces = [g[0] for g in got]
+        effs = [g[1] for g in got]
+        idxs = [g[2] for g in got] if gather else idx_parts
+    trace = sorted((k, e) for tr in traces for k, e in tr)
+    eff = next(e for e in effs if e is not None)
+    table = states(cfg.slm.scheme)
+    holos = [table[i] for part in idxs for i in part]
+    return holos, RunReport(error_trace=trace, final_error=trace[-1][1], efficiency=eff, iterations_executed=S,
+                            runtime_ms=(time.perf_counter() - start) * 1e3, seed_used=cfg.seed, termination=COMPLETED)

@@ -103,6 +103,38 @@ class GenerationPlan:
         _native.check(st)
         return rep, (tk, tv)
 
+    def ospr_part(self, streams, frame0, nframes_total, phase):
+        """One contiguous part of a subframe-sharded OSPR run
+        (cgh_plan_ospr_part): ``streams`` = the numpy SeedSequence children of
+        these frames. Returns (report, per-frame error list)."""
+        m = len(streams)
+        fr = (_native.Pcg64State * max(1, m))()
+        for i, sq in enumerate(streams):
+            fr[i] = _native.Pcg64State.from_bitgen(np.random.PCG64(sq))
+        op = _native.OsprParams(m, ctypes.cast(fr, ctypes.POINTER(_native.Pcg64State)))
+        rep = _native.Report()
+        tk = np.zeros(max(1, m), np.int64)
+        tv = np.zeros(max(1, m), np.float64)
+        _native.check(self.lib.cgh_plan_ospr_part(self.handle, ctypes.byref(op), int(frame0), int(nframes_total),
+                                                  int(phase), _native.ptr(tk), _native.ptr(tv), max(1, m),
+                                                  ctypes.byref(rep)))
+        return rep, [(int(k), float(v)) for k, v in zip(tk[:m], tv[:m])]
+
+    def intensity_ptr(self):
+        """(device address, bytes) of the plan's carried intensity plane."""
+        p, nbytes = ctypes.c_void_p(), ctypes.c_int64()
+        _native.check(self.lib.cgh_plan_intensity(self.handle, ctypes.byref(p), ctypes.byref(nbytes)))
+        return int(p.value or 0), int(nbytes.value)
+
+    def copy_intensity(self, dst_ptr):
+        """Copy the intensity plane to device address ``dst_ptr`` (H*W reals)."""
+        _native.check(self.lib.cgh_plan_copy_intensity(self.handle, ctypes.c_void_p(int(dst_ptr))))
+
+    def set_intensity(self, plane_ptrs):
+        """intensity := sum of the device planes at ``plane_ptrs`` (fixed order)."""
+        arr = (ctypes.c_void_p * max(1, len(plane_ptrs)))(*[ctypes.c_void_p(int(q)) for q in plane_ptrs])
+        _native.check(self.lib.cgh_plan_set_intensity(self.handle, arr, len(plane_ptrs)))
+
     def sa(self, seed=None, proposals=None):
         """run_sa on the resident target (plan must be FP64)."""
         cfg = self.cfg
