@@ -468,6 +468,44 @@ def run_ours(args):
       except Exception as exc:  # noqa: BLE001
         c6 = {"error": f"{type(exc).__name__}: {exc}"}
 
+    # C2 OSPR with its 24 subframes sharded over the ranks (strong scaling,
+    # one exchange of |R|^2 totals per hologram)
+    ospr_sh = None
+    if not args.no_ospr:
+      try:
+        from paper_2006_10509_b200.multi import OsprShardSession
+        from paper_2006_10509_b200.slab import SymmetricExchange, TorchExchange
+        from paper_2006_10509_b200.slm import SlmSpec as _Slm, binary_phase as _bin
+
+        scfg2 = make_cfg(1, n=OSPR_N, kind="fourier", algorithm="ospr", subframes=OSPR_S)
+        scfg2.slm = _Slm(OSPR_N, OSPR_N, _bin())
+        t2 = natural_target(OSPR_N)
+        kind2 = "none (1 GPU)"
+        exch2 = None
+        if world > 1:
+            try:
+                exch2, kind2 = SymmetricExchange(), "|R|^2 totals read through NVLink peer pointers"
+            except Exception:  # noqa: BLE001
+                exch2, kind2 = TorchExchange(), "NCCL all-gather of |R|^2 totals"
+        with device(local), precision("fp32"):
+            sess2 = OsprShardSession(scfg2, t2, exchange=exch2)
+            sess2.run()                                                            # warm
+            reps2 = max(3, min(10, args.steps // 4))
+            barrier()
+            t0 = time.perf_counter()
+            for _ in range(reps2):
+                sess2.run()
+            barrier()
+            ts2 = max_over_ranks(time.perf_counter() - t0) / reps2
+            sess2.close()
+        ospr_sh = {"metric": f"OSPR holograms/s, one C2 hologram ({OSPR_N}x{OSPR_N} binary, {OSPR_S} subframes) "
+                             f"sharded over {world} GPU(s)", "value": 1.0 / ts2, "unit": "holograms/s",
+                   "scaling": "strong", "exchange": kind2,
+                   "note": "wall time per hologram with plans and target resident (phase 1, exchange of |R|^2 "
+                           "totals, phase 2; per-frame errors on the host), max over ranks"}
+      except Exception as exc:  # noqa: BLE001
+        ospr_sh = {"error": f"{type(exc).__name__}: {exc}"}
+
     # .hgi output: payload + CRC-32 of the C3 hologram from
     # its index plane on the device vs host expansion + zlib (serialio.py:167-185)
     hgi = None
@@ -517,7 +555,8 @@ def run_ours(args):
                            "l2": "256 MB device write between timed steps (excluded from step time)"},
                 "gpu_launches": launches, "wall_s_timed": t_wall,
                 "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clk.summary(), "ospr": ospr,
-                "search": search, "c5": c5, "c6": c6, "hgi": hgi}
+                "search": search, "c5": c5, "c6": c6, "hgi": hgi,
+                "ospr_sharded": ospr_sh}
         print(json.dumps(line), flush=True)
     plan.close()
     if world > 1:

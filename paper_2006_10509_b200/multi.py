@@ -176,50 +176,81 @@ def _ospr_plane_exchange(plans, exch, rank_ids, world):
     p.set_intensity([allp[i].data_ptr() for i in range(rank)])
 
 
+class OsprShardSession:
+    """Prepared subframe-sharded OSPR run (plans and target resident);
+    ``run()`` = phase 1, the exchange of |R|^2 totals, phase 2."""
+
+    def __init__(self, cfg, target, illumination=None, *, exchange=None, precision=None, device=None):
+        import numpy as np
+
+        from .algorithms import _check_inputs
+        from .plan import GenerationPlan
+        from .slab import LocalExchange, SimulatedExchange
+
+        target = np.asarray(target, dtype=np.complex128)
+        _check_inputs(cfg, target, illumination)
+        self.cfg, self.shape = cfg, target.shape
+        self.exch = exchange or LocalExchange()
+        self.world = self.exch.world
+        self.S = int(cfg.subframes)
+        self.rank_ids = list(range(self.world)) if isinstance(self.exch, SimulatedExchange) else \
+            [getattr(self.exch, "rank", 0)]
+        self.parts = [shard(self.S, self.world, r) for r in self.rank_ids]
+        self.plans = []
+        for _ in self.rank_ids:
+            p = GenerationPlan(cfg, target.shape, precision=precision, device=device)
+            p.set_target(target, illumination)
+            self.plans.append(p)
+
+    def run(self, seed=None):
+        """Returns (this process's per-frame errors [(k, err)], efficiency or None)."""
+        import numpy as np
+
+        streams = np.random.SeedSequence(self.cfg.seed if seed is None else seed).spawn(self.S)   # algorithms.py:487
+        for p, (lo, hi) in zip(self.plans, self.parts):
+            if hi > lo:
+                p.ospr_part(streams[lo:hi], lo, self.S, 1)
+            else:
+                p.set_intensity([])
+        _ospr_plane_exchange(self.plans, self.exch, self.rank_ids, self.world)
+        trace, eff = [], None
+        for p, (lo, hi) in zip(self.plans, self.parts):
+            if hi > lo:
+                rep, tr = p.ospr_part(streams[lo:hi], lo, self.S, 2)
+                trace += tr
+                if hi == self.S:
+                    eff = float(rep.efficiency)
+        return trace, eff
+
+    def indices(self):
+        import numpy as np
+
+        return [p.download_indices(hi - lo) if hi > lo else np.empty((0,) + self.shape, np.uint8)
+                for p, (lo, hi) in zip(self.plans, self.parts)]
+
+    def close(self):
+        for p in self.plans:
+            p.close()
+
+
 def run_ospr_sharded(cfg, target, illumination=None, *, exchange=None, gather=True, precision=None, device=None):
     """``run_ospr`` (algorithms.py:473-530) with the subframes sharded over
     ranks. Returns (list of complex128 subframe holograms — all S when
     ``gather``, else this rank's part —, RunReport) on every rank."""
     import time
 
-    import numpy as np
-
-    from .algorithms import COMPLETED, RunReport, _check_inputs
-    from .plan import GenerationPlan
-    from .slab import LocalExchange, SimulatedExchange
+    from .algorithms import COMPLETED, RunReport
+    from .slab import SimulatedExchange
     from .slm import states
 
     start = time.perf_counter()
-    target = np.asarray(target, dtype=np.complex128)
-    _check_inputs(cfg, target, illumination)
-    exch = exchange or LocalExchange()
-    world = exch.world
-    S = int(cfg.subframes)
-    streams = np.random.SeedSequence(cfg.seed).spawn(S)   # algorithms.py:487
-    rank_ids = list(range(world)) if isinstance(exch, SimulatedExchange) else [getattr(exch, "rank", 0)]
-    parts = [shard(S, world, r) for r in rank_ids]
-    plans = []
-    for r, (lo, hi) in zip(rank_ids, parts):
-        p = GenerationPlan(cfg, target.shape, precision=precision, device=device)
-        p.set_target(target, illumination)
-        if hi > lo:
-            p.ospr_part(streams[lo:hi], lo, S, 1)
-        else:
-            p.set_intensity([])
-        plans.append(p)
-    _ospr_plane_exchange(plans, exch, rank_ids, world)
-    local_trace, eff, idx_parts = [], None, []
-    for p, (lo, hi) in zip(plans, parts):
-        if hi > lo:
-            rep, tr = p.ospr_part(streams[lo:hi], lo, S, 2)
-            local_trace += tr
-            if hi == S:
-                eff = float(rep.efficiency)
-            idx_parts.append(p.download_indices(hi - lo))
-        else:
-            idx_parts.append(np.empty((0,) + target.shape, np.uint8))
-    for p in plans:
-        p.close()
+    sess = OsprShardSession(cfg, target, illumination, exchange=exchange, precision=precision, device=device)
+    try:
+        local_trace, eff = sess.run()
+        idx_parts = sess.indices()
+    finally:
+        sess.close()
+    exch, world = sess.exch, sess.world
     if isinstance(exch, SimulatedExchange) or world == 1:
         traces, effs, idxs = [local_trace], [eff], idx_parts
     else:
@@ -234,5 +265,5 @@ def run_ospr_sharded(cfg, target, illumination=None, *, exchange=None, gather=Tr
     eff = next(e for e in effs if e is not None)
     table = states(cfg.slm.scheme)
     holos = [table[i] for part in idxs for i in part]
-    return holos, RunReport(error_trace=trace, final_error=trace[-1][1], efficiency=eff, iterations_executed=S,
+    return holos, RunReport(error_trace=trace, final_error=trace[-1][1], efficiency=eff, iterations_executed=sess.S,
                             runtime_ms=(time.perf_counter() - start) * 1e3, seed_used=cfg.seed, termination=COMPLETED)
