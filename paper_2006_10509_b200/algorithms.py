@@ -186,7 +186,9 @@ def _mask_bytes(cfg, target):
     mask = np.asarray(cfg.metric.mask)
     if mask.shape != target.shape:
         raise DimensionMismatchError(f"mask {mask.shape} does not match target {target.shape}")
-    return np.ascontiguousarray(mask, dtype=np.uint8)
+    if mask.dtype == np.bool_ and mask.flags.c_contiguous:
+        return mask.view(np.uint8)            # numpy bools are bytes 0/1: no copy
+    return np.ascontiguousarray(mask != 0, dtype=np.uint8)
 
 
 def _illum(illumination):

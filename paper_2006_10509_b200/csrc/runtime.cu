@@ -192,6 +192,9 @@ void plan_free(cgh_plan* P) {
         if (b->p) cudaFreeAsync(b->p, P->st);
     if (P->st) cudaStreamSynchronize(P->st);
     if (P->res_h) cudaFreeHost(P->res_h);
+    for (void* h : P->pin) cudaFreeHost(h);
+    for (auto st : P->pin_st) cudaStreamDestroy(st);
+    for (auto e : P->pin_ev) cudaEventDestroy(e);
     for (auto e : P->evpool) cudaEventDestroy(e);
     if (P->ev0) cudaEventDestroy(P->ev0);
     if (P->ev1) cudaEventDestroy(P->ev1);
@@ -238,13 +241,13 @@ static int prep_target(cgh_plan* P, const double* target, const uint8_t* mask, c
     CGH_TRY(ensure(P, P->stage, size_t(n) * 16 * (illum ? 2 : 1)));
     CGH_TRY(ensure(P, P->mask, size_t(n)));
     CGH_TRY(ensure(P, P->tgt, size_t(n) * sizeof(T)));
-    CGH_CUDA(cudaMemcpyAsync(P->stage.p, target, size_t(n) * 16, cudaMemcpyHostToDevice, P->st));
+    CGH_TRY(upload_staged(P, P->stage.p, target, size_t(n) * 16));
     CGH_CUDA(cudaMemcpyAsync(P->mask.p, mask, size_t(n), cudaMemcpyHostToDevice, P->st));
     double* ic = nullptr;
     if (illum) {
         ic = static_cast<double*>(P->stage.p) + 2 * n;
         CGH_TRY(ensure(P, P->beam, size_t(n) * sizeof(T)));
-        CGH_CUDA(cudaMemcpyAsync(ic, illum, size_t(n) * 16, cudaMemcpyHostToDevice, P->st));
+        CGH_TRY(upload_staged(P, ic, illum, size_t(n) * 16));
     }
     P->has_beam = illum != nullptr;
     const int grid = grid_for(n);
@@ -268,6 +271,69 @@ static int prep_target(cgh_plan* P, const double* target, const uint8_t* mask, c
     P->nf_beam = st[4];
     P->target_ready = true;
     fast_invalidate_target(P);
+    return CGH_OK;
+}
+
+constexpr int kStageThreads = 4;
+constexpr size_t kStageChunk = size_t(4) << 20;   // bytes per pinned chunk (2 per thread)
+
+int upload_staged(cgh_plan* P, void* dst, const void* src, size_t bytes) {
+    if (bytes < (size_t(16) << 20)) {
+        CGH_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, P->st));
+        return CGH_OK;
+    }
+    if (P->pin.empty()) {
+        for (int i = 0; i < 2 * kStageThreads; ++i) {
+            void* h = nullptr;
+            CGH_CUDA(cudaHostAlloc(&h, kStageChunk, cudaHostAllocDefault));
+            P->pin.push_back(h);
+            cudaEvent_t e;
+            CGH_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            P->pin_ev.push_back(e);
+        }
+        for (int t = 0; t < kStageThreads; ++t) {
+            cudaStream_t st;
+            CGH_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+            P->pin_st.push_back(st);
+        }
+        cudaEvent_t e;   // start event (last slot)
+        CGH_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        P->pin_ev.push_back(e);
+    }
+    // pinned chunks still being read by an earlier upload's DMAs
+    for (int i = 0; i < 2 * kStageThreads; ++i) CGH_CUDA(cudaEventSynchronize(P->pin_ev[i]));
+    // the staging streams start after earlier work on P->st (dst may be in use)
+    cudaEvent_t start = P->pin_ev[2 * kStageThreads];
+    CGH_CUDA(cudaEventRecord(start, P->st));
+    for (int t = 0; t < kStageThreads; ++t) CGH_CUDA(cudaStreamWaitEvent(P->pin_st[t], start, 0));
+    const size_t slice = (bytes + kStageThreads - 1) / kStageThreads;
+    std::atomic<int> err{0};
+    auto worker = [&](int t) {
+        cudaSetDevice(P->dev);
+        const size_t lo = std::min(bytes, size_t(t) * slice), hi = std::min(bytes, lo + slice);
+        int k = 0;
+        for (size_t off = lo; off < hi; off += kStageChunk, ++k) {
+            const int b = 2 * t + (k & 1);
+            const size_t len = std::min(kStageChunk, hi - off);
+            if (k >= 2 && cudaEventSynchronize(P->pin_ev[b]) != cudaSuccess) err = 1;   // chunk's previous DMA done
+            memcpy(P->pin[b], static_cast<const char*>(src) + off, len);
+            if (cudaMemcpyAsync(static_cast<char*>(dst) + off, P->pin[b], len, cudaMemcpyHostToDevice,
+                                P->pin_st[t]) != cudaSuccess)
+                err = 1;
+            if (cudaEventRecord(P->pin_ev[b], P->pin_st[t]) != cudaSuccess) err = 1;
+        }
+    };
+    std::vector<std::thread> th;
+    for (int t = 1; t < kStageThreads; ++t) th.emplace_back(worker, t);
+    worker(0);
+    for (auto& x : th) x.join();
+    if (err) return fail(CGH_ERR_CUDA, "staged upload failed");
+    for (int t = 0; t < kStageThreads; ++t) {
+        CGH_CUDA(cudaEventRecord(P->pin_ev[2 * t], P->pin_st[t]));
+        CGH_CUDA(cudaStreamWaitEvent(P->st, P->pin_ev[2 * t], 0));
+    }
+    // pinned chunks are reused by the next upload only after these DMAs: the
+    // next call records `start` on P->st, which now waits for them
     return CGH_OK;
 }
 

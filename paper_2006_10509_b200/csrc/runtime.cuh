@@ -72,6 +72,10 @@ struct cgh_plan {
     bool has_beam = false, target_ready = false;
     // mapped host results
     double* res_h = nullptr;
+    // pinned staging for large host->device uploads (upload_staged)
+    std::vector<void*> pin;
+    std::vector<cudaStream_t> pin_st;
+    std::vector<cudaEvent_t> pin_ev;
     double* res_d = nullptr;
     size_t res_cap = 0;
     // prep statistics
@@ -96,6 +100,10 @@ int ensure(cgh_plan* P, DevBuf& b, size_t bytes);
 int ensure_res(cgh_plan* P, size_t n);
 int ensure_events(cgh_plan* P, size_t n);
 int plan_upload_target(cgh_plan* P, const double* target, const uint8_t* mask, const double* illum);
+// Host -> device copy of a large pageable buffer through pinned staging:
+// host threads copy slices into double-buffered pinned chunks and issue the
+// DMAs on their own streams; P->st waits for them. Small copies go direct.
+int upload_staged(cgh_plan* P, void* dst, const void* src, size_t bytes);
 
 template <class T>
 PassArgs<T> base_args(cgh_plan* P);
