@@ -309,8 +309,8 @@ def run_ours(args):
             te = max_over_ranks(time.perf_counter() - t0)
         e2e = {"value": world * ke * ITERS / te, "unit": "iter/s",
                "h2d_bytes_per_step": hw * 16 + hw, "d2h_bytes_per_step": hw * 1 + (ITERS + 1) * 16,
-               "note": "run_gs(cfg, numpy complex128 target) per step: pageable H2D of target+mask, "
-                       "D2H of the uint8 index plane, host states[idx] expansion"}
+               "note": "run_gs(cfg, numpy complex128 target) per step: H2D of target (pinned staging by 4 host "
+                       "threads) + mask, D2H of the uint8 index plane, host states[idx] expansion"}
 
     # OSPR holograms/s, resident target: C2 (1024^2 binary, 24 subframes) and
     # the metric's 2048^2 size (binary, 24 subframes)
