@@ -152,7 +152,9 @@ __device__ __forceinline__ cx<T> holo_project(const PassArgs<T>& a, cx<T> x, int
     const T mag2 = x.x * x.x + x.y * x.y;
     cx<T> h;
     if (mag2 > T(0)) {
-        const T inv = amp / dev_sqrt<T>(mag2);
+        T inv;
+        if constexpr (sizeof(T) == 4) inv = amp * rsqrtf(mag2);   // as the fast row pass
+        else inv = amp / dev_sqrt<T>(mag2);
         h = mk(x.x * inv, x.y * inv);
     } else {
         h = mk(amp, T(0));

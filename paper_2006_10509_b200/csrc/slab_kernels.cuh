@@ -179,32 +179,58 @@ __global__ void __launch_bounds__(SlabShape<T, N>::THREADS) slab_kernel(SlabArgs
                 slab_fft<T, N, -1>(v, sre, sim, t, smem, a.p.tw_row);
                 const T gain = a.gain;
                 T sdd = 0, srr = 0, srd = 0, sall = 0;
+                if constexpr (sizeof(T) == 4) {
+                    // branchless fp32 form of the fast column pass (fast_col_gs):
+                    // |R| = r2 * rsqrt(r2), projection scale = want * rsqrt(r2)
 #pragma unroll
-                for (int r = 0; r < E; ++r) {
-                    const int u = t + r * TF;
-                    const cx<T> Rv = v[r] * a.scale;
-                    const T r2 = Rv.x * Rv.x + Rv.y * Rv.y;
-                    const T rr = dev_sqrt<T>(r2);
-                    const T tt = active ? a.tgt[long(i) * N + u] : T(-0.0);
-                    sall += active ? r2 : T(0);
-                    cx<T> out = Rv;
-                    if (!signbit(tt)) {
-                        const T d = rr - tt;
-                        sdd += d * d;
-                        srr += r2;
-                        srd += rr * d;
+                    for (int r = 0; r < E; ++r) {
+                        const int u = t + r * TF;
+                        const cx<T> Rv = v[r] * a.scale;
+                        const float r2 = Rv.x * Rv.x + Rv.y * Rv.y;
+                        const float ri = rsqrtf(r2);                 // inf at 0
+                        const float rr = r2 > 0.0f ? r2 * ri : 0.0f;
+                        const float tt = active ? a.tgt[long(i) * N + u] : -0.0f;
+                        const bool in = !signbit(tt);
+                        const float d = rr - tt;
+                        sall += active ? r2 : 0.0f;
+                        sdd += in ? d * d : 0.0f;
+                        srr += in ? r2 : 0.0f;
+                        srd += in ? rr * d : 0.0f;
                         if constexpr (mode == SLAB_GS) {
-                            T want = tt + gain * (tt - rr);
-                            want = want > T(0) ? want : T(0);
-                            if (rr > T(0)) {
-                                const T s = want / rr;
-                                out = mk(Rv.x * s, Rv.y * s);
-                            } else {
-                                out = mk(want, T(0));
-                            }
+                            const float want = fmaxf(tt + gain * (tt - rr), 0.0f);
+                            const bool pos = r2 > 0.0f;
+                            const float kk = in ? (pos ? want * ri : 0.0f) : 1.0f;
+                            v[r] = mk(Rv.x * kk + ((in && !pos) ? want : 0.0f), Rv.y * kk);
                         }
                     }
-                    v[r] = out;
+                } else {
+#pragma unroll
+                    for (int r = 0; r < E; ++r) {
+                        const int u = t + r * TF;
+                        const cx<T> Rv = v[r] * a.scale;
+                        const T r2 = Rv.x * Rv.x + Rv.y * Rv.y;
+                        const T rr = dev_sqrt<T>(r2);
+                        const T tt = active ? a.tgt[long(i) * N + u] : T(-0.0);
+                        sall += active ? r2 : T(0);
+                        cx<T> out = Rv;
+                        if (!signbit(tt)) {
+                            const T d = rr - tt;
+                            sdd += d * d;
+                            srr += r2;
+                            srd += rr * d;
+                            if constexpr (mode == SLAB_GS) {
+                                T want = tt + gain * (tt - rr);
+                                want = want > T(0) ? want : T(0);
+                                if (rr > T(0)) {
+                                    const T sc = want / rr;
+                                    out = mk(Rv.x * sc, Rv.y * sc);
+                                } else {
+                                    out = mk(want, T(0));
+                                }
+                            }
+                        }
+                        v[r] = out;
+                    }
                 }
                 dsdd += double(sdd);
                 dsrr += double(srr);
