@@ -94,13 +94,15 @@ __device__ __forceinline__ int quantize_index(const SchemeDev& s, cx<T> z) {
         const T frac = py_mod<T>((ang - T(s.offset)) / T(s.step), T(L));
         const T lowf = floor(frac);
         const T rem = frac - lowf;
-        long low = (long)lowf;
-        long high = (low + 1) % L;
-        long pick = rem < T(0.5) ? low : high;
+        // 0 <= frac < L, so 32-bit integer wrap-around gives the same indices
+        // as the 64-bit form (and avoids 64-bit % on the GPU)
+        const int low = int(lowf);
+        const int high = low + 1 == L ? 0 : low + 1;
+        int pick = rem < T(0.5) ? low : high;
         if (rem == T(0.5)) pick = low < high ? low : high;
-        pick %= L;
+        if (pick >= L) pick -= L;
         if (pick < 0) pick += L;
-        return int(pick);
+        return pick;
     }
     // generic nearest by Euclidean distance, first minimum wins
     int best = 0;
