@@ -318,7 +318,55 @@ __global__ void __launch_bounds__(kSearchThreads, 1) dbs_kernel(SearchArgs a) {
             }
             __syncthreads();
         }
-        for (int k = 0; k < W; ++k) {
+        if (Lv == 2) {
+            // binary schemes: one valid level per candidate (the other state).
+            // Candidates in chunks of 8 share one pass over the slice, so R, t
+            // and |R| are read/computed once per element per chunk; each
+            // candidate's per-thread sum has the same terms in the same order
+            // as the per-candidate loop below (identical decisions).
+            constexpr int KC = 8;
+            for (int k0 = 0; k0 < W; k0 += KC) {
+                double acc[KC];
+#pragma unroll
+                for (int kk = 0; kk < KC; ++kk) acc[kk] = 0.0;
+                for (long long li = threadIdx.x; li < s.count; li += blockDim.x) {
+                    int mu, mv;
+                    element_pos(a, s, li, mu, mv);
+                    const double2 R = s.R[li];
+                    const double t = s.t[li];
+                    const double d0 = dabs(R) - t;
+                    const double b0 = d0 * d0;
+#pragma unroll
+                    for (int kk = 0; kk < KC; ++kk) {
+                        const int k = k0 + kk;
+                        if (k < W) {
+                            const int jv = wvalid[k * 2] ? 0 : 1;
+                            if (wvalid[k * 2 + jv]) {
+                                const double2 w = tw_of(L.rt, L.ct, a, wm[k], wn[k], mu, mv);
+                                const double2 u = dmul(wd[k * 2 + jv], w);
+                                const double d1 = dabs(make_double2(R.x + u.x, R.y + u.y)) - t;
+                                acc[kk] += d1 * d1 - b0;
+                            }
+                        }
+                    }
+                }
+#pragma unroll
+                for (int kk = 0; kk < KC; ++kk) {
+                    const int k = k0 + kk;
+                    if (k < W) {
+                        double v = acc[kk];
+#pragma unroll
+                        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                        if (lane == 0) {
+                            const int jv = wvalid[k * 2] ? 0 : 1;
+                            wsum[warp * NQMAX + k * 2 + jv] = v;
+                            wsum[warp * NQMAX + k * 2 + (1 - jv)] = 0.0;
+                        }
+                    }
+                }
+            }
+        }
+        for (int k = 0; k < (Lv == 2 ? 0 : W); ++k) {
             double acc[kMaxLevels];
 #pragma unroll
             for (int j = 0; j < kMaxLevels; ++j) acc[j] = 0.0;
