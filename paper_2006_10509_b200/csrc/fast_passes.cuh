@@ -854,10 +854,8 @@ __global__ void __launch_bounds__(TH, MINB) fast_ospr_gen(FastOsprArgs a) {
         const float* trow = a.tgt + size_t(u) * N;
 #pragma unroll 4
         for (int e = 0; e < 16; ++e) {
-            double x = 2.0 * pcg_next_double(gen);   // angle / pi in [0, 2)
-            if (x > 1.0) x -= 2.0;
             float sn, cs;
-            sincospif(float(x), &sn, &cs);
+            sincospif(pcg_next_halfturns(gen), &sn, &cs);   // angle / pi in [-1, 1)
             const int pos = (16 * t + e + N / 2) & (N - 1);   // uncentred column of centred 16t+e
             const float amp = fabsf(trow[pos]);
             line[padc(pos)] = make_float2(amp * cs, amp * sn);

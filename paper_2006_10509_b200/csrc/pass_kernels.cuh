@@ -16,17 +16,15 @@ __device__ __forceinline__ double* red_scratch(unsigned char* smem, size_t fft_b
 // Random-phase start value of hologram pixel index p (row-major draw p).
 template <class T>
 __device__ __forceinline__ cx<T> unit_phase(Pcg64& g) {
-    const double u = pcg_next_double(g);
     if constexpr (sizeof(T) == 8) {
+        const double u = pcg_next_double(g);
         const double theta = 6.283185307179586 * u;   // 2.0 * np.pi * u
         double s, c;
         sincos(theta, &s, &c);
         return mk<T>(c, s);
     } else {
-        double x = 2.0 * u;               // angle / pi in [0, 2)
-        if (x > 1.0) x -= 2.0;            // exact; |x| <= 1
         float s, c;
-        sincospif(float(x), &s, &c);
+        sincospif(pcg_next_halfturns(g), &s, &c);   // angle / pi in [-1, 1)
         return mk<T>(c, s);
     }
 }

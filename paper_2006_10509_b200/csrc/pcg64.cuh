@@ -38,6 +38,16 @@ __host__ __device__ __forceinline__ double pcg_next_double(Pcg64& g) {
     return double(pcg_next64(g) >> 11) * (1.0 / 9007199254740992.0);
 }
 
+// float(x) for x = 2u, shifted to [-1, 1) (x - 2 when x > 1), u = next_double:
+// the same value as float((2.0 * u > 1.0) ? 2.0 * u - 2.0 : 2.0 * u) computed in
+// fp64 (u = x53 * 2^-53 exactly, the shift is exact, and rounding commutes with
+// the power-of-two scale), without fp64 arithmetic.
+__host__ __device__ __forceinline__ float pcg_next_halfturns(Pcg64& g) {
+    const long long x53 = (long long)(pcg_next64(g) >> 11);
+    const long long xi = x53 > (1LL << 52) ? x53 - (1LL << 53) : x53;
+    return float(xi) * 2.220446049250313e-16f;   // 2^-52
+}
+
 __host__ __device__ __forceinline__ uint32_t pcg_next32(Pcg64& g) {
     if (g.has_uint32) {
         g.has_uint32 = 0;
