@@ -45,6 +45,8 @@ OSPR_N = 1024
 OSPR_S = 24
 C5_N, C5_TARGETS, C5_ITERS = 4096, 64, 100   # batched GS (100 iterations)
 C6_N, C6_ITERS = 16384, 20                   # distributed GS (§8d: "C6 timing may use 20 iterations")
+# tests: take the collective code paths (symmetric memory / NCCL) even with one rank
+FORCE_DIST = os.environ.get("CGHB200_BENCH_FORCE_DIST") == "1"
 METRIC = "GS iterations/s (Fresnel 2048x2048, PhaseOnly(8), 200 iterations per run)"
 
 
@@ -199,7 +201,7 @@ def run_ours(args):
     import torch
 
     torch.cuda.set_device(local)
-    if world > 1:
+    if world > 1 or FORCE_DIST:
         import torch.distributed as dist
 
         import datetime
@@ -209,7 +211,7 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local), timeout=datetime.timedelta(minutes=3))
 
     def barrier():
-        if world > 1:
+        if world > 1 or FORCE_DIST:
             torch.distributed.barrier()
         torch.cuda.synchronize()
 
@@ -429,7 +431,7 @@ def run_ours(args):
         target6 = natural_target(C6_N)
         exch_kind = "none (G = 1: local block transposes)"
         sess = None
-        if world > 1:
+        if world > 1 or FORCE_DIST:
             try:   # NVLink peer stores from the fused turn kernel (torch symmetric memory)
                 sess = SL.SlabSession(c6cfg, target6, exchange=SL.SymmetricExchange(), precision=_native.FP32,
                                       device=local)
@@ -482,7 +484,7 @@ def run_ours(args):
         t2 = natural_target(OSPR_N)
         kind2 = "none (1 GPU)"
         exch2 = None
-        if world > 1:
+        if world > 1 or FORCE_DIST:
             try:
                 exch2, kind2 = SymmetricExchange(), "|R|^2 totals read through NVLink peer pointers"
             except Exception:  # noqa: BLE001
@@ -559,7 +561,7 @@ def run_ours(args):
                 "ospr_sharded": ospr_sh}
         print(json.dumps(line), flush=True)
     plan.close()
-    if world > 1:
+    if world > 1 or FORCE_DIST:
         torch.distributed.destroy_process_group()
 
 

@@ -127,7 +127,7 @@ def run_sharded(jobs, runner=None, group=None, device_index=None, keep_holograms
     return [r for part in gathered for r in part]
 
 
-def _ospr_plane_exchange(plans, exch, rank_ids, world):
+def _ospr_plane_exchange(plans, exch, rank_ids, world, cache=None):
     """Phase-1 totals -> each rank's base = sum of the lower ranks' totals.
 
     SimulatedExchange: the planes are the other virtual ranks' intensity
@@ -161,9 +161,12 @@ def _ospr_plane_exchange(plans, exch, rank_ids, world):
     if isinstance(exch, SymmetricExchange):
         import torch.distributed._symmetric_memory as symm
 
-        plane = symm.empty(n_el, dtype=dt, device=dev)
-        group = exch.group if exch.group is not None else exch.dist.group.WORLD
-        h = symm.rendezvous(plane, group)
+        cache = {} if cache is None else cache
+        if "symm" not in cache:   # one symmetric plane per session (rendezvous is a collective)
+            plane = symm.empty(n_el, dtype=dt, device=dev)
+            group = exch.group if exch.group is not None else exch.dist.group.WORLD
+            cache["symm"] = (plane, symm.rendezvous(plane, group))
+        plane, h = cache["symm"]
         p.copy_intensity(plane.data_ptr())
         h.barrier(channel=0)
         p.set_intensity(list(h.buffer_ptrs)[:rank])
@@ -197,6 +200,7 @@ class OsprShardSession:
             [getattr(self.exch, "rank", 0)]
         self.parts = [shard(self.S, self.world, r) for r in self.rank_ids]
         self.plans = []
+        self._xcache = {}
         for _ in self.rank_ids:
             p = GenerationPlan(cfg, target.shape, precision=precision, device=device)
             p.set_target(target, illumination)
@@ -212,7 +216,7 @@ class OsprShardSession:
                 p.ospr_part(streams[lo:hi], lo, self.S, 1)
             else:
                 p.set_intensity([])
-        _ospr_plane_exchange(self.plans, self.exch, self.rank_ids, self.world)
+        _ospr_plane_exchange(self.plans, self.exch, self.rank_ids, self.world, self._xcache)
         trace, eff = [], None
         for p, (lo, hi) in zip(self.plans, self.parts):
             if hi > lo:
