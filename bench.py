@@ -27,13 +27,11 @@ import os
 import statistics
 import subprocess
 import sys
-import threading
 import time
 
 REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
-import numpy as np  # noqa: E402
 
 N_PX = 2048
 ITERS = 200

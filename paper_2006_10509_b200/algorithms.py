@@ -26,7 +26,7 @@ import numpy as np
 
 from . import _native
 from .errors import DimensionMismatchError
-from .propagation import FRESNEL, MetricSpec, PropagationSpec, fill_propagation, propagate_inverse
+from .propagation import FRESNEL, MetricSpec, PropagationSpec, fill_propagation, propagate_inverse  # noqa: F401 (FRESNEL: reference namespace)
 from .runtime import current_device, runner_precision
 from .slm import SlmSpec, problem_for, states
 

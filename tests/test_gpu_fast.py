@@ -10,7 +10,7 @@ import golden_cases as G
 from oracle import cgh_oracle as O
 from paper_2006_10509_b200 import algorithms as A
 from paper_2006_10509_b200.image import rect_mask
-from paper_2006_10509_b200.propagation import FRESNEL, MetricSpec, PropagationSpec
+from paper_2006_10509_b200.propagation import MetricSpec, PropagationSpec
 from paper_2006_10509_b200.runtime import precision
 from paper_2006_10509_b200.slm import PhaseOnly, SlmSpec, states
 from paper_2006_10509_b200.workloads import gaussian_beam, natural_target

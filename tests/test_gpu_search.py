@@ -14,7 +14,6 @@ import golden_cases as G
 from oracle import cgh_oracle as O
 from paper_2006_10509_b200 import algorithms as A
 from paper_2006_10509_b200 import kernels as K
-from paper_2006_10509_b200 import propagation as P
 from paper_2006_10509_b200.search import dbs_call, sa_call
 from paper_2006_10509_b200.slm import binary_phase, states
 
