@@ -61,10 +61,6 @@ struct SlabArgs {
     ReduceArgs red;       // out[0..3] = S_dd, S_rr, S_rd, S_all of this rank
 };
 
-__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
-
 template <class T, int N, int DIR>
 __device__ __forceinline__ void slab_fft(cx<T> (&v)[SlabShape<T, N>::E], T* sre, T* sim, int t,
                                          const unsigned char* smem, const cx<T>* tw) {
@@ -77,9 +73,10 @@ __device__ __forceinline__ void slab_fft(cx<T> (&v)[SlabShape<T, N>::E], T* sre,
     }
 }
 
-// Persistent: CTA b transforms line groups b, b + gridDim.x, ... and asks L2
-// for its next group (all segments, and the target / beam rows) before
-// working on the current one, so the next loads hit L2 instead of HBM.
+// Persistent: CTA b transforms line groups b, b + gridDim.x, ... (tables set
+// up once per CTA). An L2 bulk prefetch of each CTA's next line was measured
+// to double the pass's DRAM traffic (prefetched lines evicted before use) and
+// to cost 5% at 16384^2, so lines are loaded on demand.
 template <class T, int N, int MODE>
 __global__ void __launch_bounds__(SlabShape<T, N>::THREADS) slab_kernel(SlabArgs<T> a) {
     using Sh = SlabShape<T, N>;
@@ -91,7 +88,6 @@ __global__ void __launch_bounds__(SlabShape<T, N>::THREADS) slab_kernel(SlabArgs
     T* sim = sre + WORDS;
     double* rs = red_scratch<T>(smem, Sh::FFT_BYTES);
     const int S = 1 << a.logS;
-    const int G = N >> a.logS;
 
     if constexpr (Sh::SPLIT_TW) {
         cx<T>* tws = reinterpret_cast<cx<T>*>(smem + Sh::TW_OFF);
@@ -105,17 +101,6 @@ __global__ void __launch_bounds__(SlabShape<T, N>::THREADS) slab_kernel(SlabArgs
         const int i = base + li;
         const bool active = i < a.R;
         auto at = [&](int n) -> long { return (long((n >> a.logS)) * a.R + i) * S + (n & (S - 1)); };
-        {   // L2 prefetch of the next line group of this CTA
-            const int nb = base + gridDim.x * Sh::LINES;
-            const int k = threadIdx.x;
-            if (k < Sh::LINES * G && nb + k / G < a.R) {
-                const int ni = nb + k / G, g = k % G;
-                if (mode != SLAB_INIT) prefetch_l2(a.data + (long(g) * a.R + ni) * S, uint32_t(S) * sizeof(cx<T>));
-                if (g == 0 && (mode == SLAB_GS || mode == SLAB_FINAL)) prefetch_l2(a.tgt + long(ni) * N, N * sizeof(T));
-                if (g == 0 && (mode == SLAB_INIT || mode == SLAB_HOLO) && a.p.beam)
-                    prefetch_l2(a.p.beam + long(ni) * N, N * sizeof(T));
-            }
-        }
         __syncthreads();   // shared line buffers / twiddles ready, previous line done
         cx<T> v[E];
 
