@@ -142,7 +142,9 @@ __device__ __forceinline__ int quantize_index(const SchemeDev& s, cx<T> z) {
 // Hologram-plane projection at pixel (m, n) of x = inverse-transform value
 // (unscaled): h = beam * exp(i angle(x conj q)) [-> snap] -> h q.
 // Mirrors algorithms.py:181-184 / 500-501 (propagate_inverse, angle, quantize).
-template <class T>
+// SNAP = false compiles out the snapping and field-export branches (callers
+// that know a.quantize == 0 and a.field_out == nullptr).
+template <class T, bool SNAP = true>
 __device__ __forceinline__ cx<T> holo_project(const PassArgs<T>& a, cx<T> x, int m, int n, long frame_off) {
     cx<T> q;
     const bool fres = a.q_row != nullptr;
@@ -161,8 +163,8 @@ __device__ __forceinline__ cx<T> holo_project(const PassArgs<T>& a, cx<T> x, int
     } else {
         h = mk(amp, T(0));
     }
-    if (a.field_out) a.field_out[(long)m * a.W + n] = h;
-    if (a.quantize) {
+    if (SNAP && a.field_out) a.field_out[(long)m * a.W + n] = h;
+    if (SNAP && a.quantize) {
         const int k = quantize_index<T>(a.scheme, h);
         if (a.idx_out) {
             const long p = frame_off + (long)m * a.W + n;

@@ -28,6 +28,7 @@ enum SlabMode {
     SLAB_GS = 2,      // forward -> error sums + replay projection -> inverse  (column pass of GS)
     SLAB_FINAL = 3,   // forward -> error + efficiency sums (no store)
     SLAB_INV = 4,     // inverse, scaled (backpropagation start)
+    SLAB_HOLO_SNAP = 5,   // internal: SLAB_HOLO with snapping (chosen by slab_launch_n when quantize is set)
 };
 
 template <class T, int N>
@@ -46,7 +47,9 @@ struct SlabShape {
     static constexpr int TW_WORDS = SPLIT_TW ? ((N >> TW_SH) + (1 << TW_SH)) : 0;
     static constexpr size_t FFT_BYTES = size_t(LINES) * 2 * WORDS * sizeof(T);
     static constexpr size_t TW_OFF = (FFT_BYTES + 16 + 32 * 4 * sizeof(double) + 15) / 16 * 16;
-    static constexpr size_t SMEM = TW_OFF + size_t(TW_WORDS) * sizeof(cx<T>);
+    // per-thread fp64 error-sum slots (kept out of registers across the FFTs)
+    static constexpr size_t ACC_OFF = (TW_OFF + size_t(TW_WORDS) * sizeof(cx<T>) + 15) / 16 * 16;
+    static constexpr size_t SMEM = ACC_OFF + 4 * size_t(THREADS) * sizeof(double);
 };
 
 template <class T>
@@ -95,7 +98,12 @@ __global__ void __launch_bounds__(SlabShape<T, N>::THREADS) slab_kernel(SlabArgs
         for (int k = threadIdx.x; k < NH + NL; k += blockDim.x)
             tws[k] = k < NH ? ldg_cx(a.p.tw_row + (k << Sh::TW_SH)) : ldg_cx(a.p.tw_row + (k - NH));
     }
-    double dsdd = 0, dsrr = 0, dsrd = 0, dsall = 0;   // SLAB_GS / SLAB_FINAL sums over this CTA's lines
+    // SLAB_GS / SLAB_FINAL: this thread's sums over its lines, slot q at acc[q * THREADS]
+    double* acc_sh = reinterpret_cast<double*>(smem + Sh::ACC_OFF) + threadIdx.x;
+    if constexpr (mode == SLAB_GS || mode == SLAB_FINAL) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc_sh[q * Sh::THREADS] = 0.0;
+    }
 
     for (int base = blockIdx.x * Sh::LINES; base < a.R; base += gridDim.x * Sh::LINES) {
         const int i = base + li;
@@ -149,11 +157,26 @@ __global__ void __launch_bounds__(SlabShape<T, N>::THREADS) slab_kernel(SlabArgs
         } else {
 #pragma unroll
             for (int r = 0; r < E; ++r) v[r] = active ? a.data[at(t + r * TF)] : mk<T>(0, 0);
-            if constexpr (mode == SLAB_HOLO) {
+            if constexpr (mode == SLAB_HOLO || mode == SLAB_HOLO_SNAP) {
+                // the snapping code stays out of the iteration kernel (its
+                // 32-fold unrolled quantizer cost instruction-cache misses)
                 slab_fft<T, N, +1>(v, sre, sim, t, smem, a.p.tw_row);
                 if (active) {
+                    if (mode == SLAB_HOLO && !a.p.q_row && !a.p.beam) {
+                        // Fourier, uniform beam: h = x/|x| (0 -> 1), holo_project's arithmetic with amp = 1
 #pragma unroll
-                    for (int r = 0; r < E; ++r) v[r] = holo_project<T>(a.p, v[r], i, t + r * TF, 0);
+                        for (int r = 0; r < E; ++r) {
+                            const T mag2 = v[r].x * v[r].x + v[r].y * v[r].y;
+                            T inv;
+                            if constexpr (sizeof(T) == 4) inv = rsqrtf(mag2);
+                            else inv = T(1) / dev_sqrt<T>(mag2);
+                            v[r] = mag2 > T(0) ? mk(v[r].x * inv, v[r].y * inv) : mk<T>(1, 0);
+                        }
+                    } else {
+#pragma unroll
+                        for (int r = 0; r < E; ++r)
+                            v[r] = holo_project<T, mode == SLAB_HOLO_SNAP>(a.p, v[r], i, t + r * TF, 0);
+                    }
                 }
                 slab_fft<T, N, -1>(v, sre, sim, t, smem, a.p.tw_row);
             } else if constexpr (mode == SLAB_INV) {
@@ -217,20 +240,28 @@ __global__ void __launch_bounds__(SlabShape<T, N>::THREADS) slab_kernel(SlabArgs
                         v[r] = out;
                     }
                 }
-                dsdd += double(sdd);
-                dsrr += double(srr);
-                dsrd += double(srd);
-                dsall += double(sall);
+                acc_sh[0] += double(sdd);
+                acc_sh[Sh::THREADS] += double(srr);
+                acc_sh[2 * Sh::THREADS] += double(srd);
+                acc_sh[3 * Sh::THREADS] += double(sall);
                 if constexpr (mode == SLAB_GS) slab_fft<T, N, +1>(v, sre, sim, t, smem, a.p.tw_row);
             }
         }
         if (mode != SLAB_FINAL && active) {
+            // store addresses recomputed from an opaque copy of the line index so
+            // the compiler does not keep the E load addresses live across the FFTs
+            int io;
+            asm volatile("mov.b32 %0, %1;" : "=r"(io) : "r"(i));
+            const int So = 1 << a.logS;
 #pragma unroll
-            for (int r = 0; r < E; ++r) a.data[at(t + r * TF)] = v[r];
+            for (int r = 0; r < E; ++r) {
+                const int n = t + r * TF;
+                a.data[(long((n >> a.logS)) * a.R + io) * So + (n & (So - 1))] = v[r];
+            }
         }
     }
     if constexpr (mode == SLAB_GS || mode == SLAB_FINAL) {
-        double acc[4] = {dsdd, dsrr, dsrd, dsall};
+        double acc[4] = {acc_sh[0], acc_sh[Sh::THREADS], acc_sh[2 * Sh::THREADS], acc_sh[3 * Sh::THREADS]};
         block_reduce<4>(acc, rs);
         const int nblocks = gridDim.x;
         if (publish_partials<4>(a.red, acc, nblocks, blockIdx.x)) {
@@ -324,7 +355,8 @@ template <class T, int N>
 cudaError_t slab_launch_n(const SlabArgs<T>& a, int mode, cudaStream_t st) {
     switch (mode) {
         case SLAB_INIT: return slab_launch_m<T, N, SLAB_INIT>(a, st);
-        case SLAB_HOLO: return slab_launch_m<T, N, SLAB_HOLO>(a, st);
+        case SLAB_HOLO:
+            return a.p.quantize ? slab_launch_m<T, N, SLAB_HOLO_SNAP>(a, st) : slab_launch_m<T, N, SLAB_HOLO>(a, st);
         case SLAB_GS: return slab_launch_m<T, N, SLAB_GS>(a, st);
         case SLAB_FINAL: return slab_launch_m<T, N, SLAB_FINAL>(a, st);
         case SLAB_INV: return slab_launch_m<T, N, SLAB_INV>(a, st);
