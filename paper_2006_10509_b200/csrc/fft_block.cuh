@@ -13,6 +13,7 @@
 // host (conjugated for the inverse). Stages exchange through shared memory
 // stored as split re/im arrays with one pad word per 128 bytes.
 #pragma once
+#include <type_traits>
 #include "cx.cuh"
 
 namespace cgh {
@@ -153,10 +154,24 @@ struct LineFft {
             for (int b = 0; b < NB; ++b) {
                 const int j = t + b * TF;
                 const int jm = j & (NS - 1);
+                if constexpr (std::is_same<TWS, TwSplit<T>>::value) {
+                    // split table: look up w^r for r = 1, 5, 9, ... and step the
+                    // three powers in between by w (at most 3 extra roundings;
+                    // a quarter of the shared-memory lookups)
+                    const int k = jm * (N / (NS * R));
+                    const cx<T> w1 = tw_at<T>(tw, k);
+                    cx<T> w = w1;
 #pragma unroll
-                for (int r = 1; r < R; ++r) {
-                    cx<T> w = tw_at<T>(tw, jm * r * (N / (NS * R)));
-                    v[b * R + r] = DIR < 0 ? cmul(v[b * R + r], w) : cmulc(v[b * R + r], w);
+                    for (int r = 1; r < R; ++r) {
+                        if (r > 1) w = (r & 3) == 1 ? tw_at<T>(tw, k * r) : cmul(w, w1);
+                        v[b * R + r] = DIR < 0 ? cmul(v[b * R + r], w) : cmulc(v[b * R + r], w);
+                    }
+                } else {
+#pragma unroll
+                    for (int r = 1; r < R; ++r) {
+                        cx<T> w = tw_at<T>(tw, jm * r * (N / (NS * R)));
+                        v[b * R + r] = DIR < 0 ? cmul(v[b * R + r], w) : cmulc(v[b * R + r], w);
+                    }
                 }
             }
         }
