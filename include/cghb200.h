@@ -279,6 +279,10 @@ int cgh_delta_replay_update(int32_t device, double *replay, int32_t h, int32_t w
  * hologram of every runner) with `threads` host threads (no GPU needed). */
 int cgh_expand_states(const void *idx, int32_t idx_bytes, int64_t count, const double *states, int32_t n_states,
                       double *out, int32_t threads);
+/* ---- host: touch one byte per 4 KB page of [p, p + bytes) (writes zeros)
+ * with `threads` host threads, so a fresh output array is faulted in while the
+ * device runs instead of during cgh_expand_states. No reference counterpart. */
+int cgh_prefault(void *p, int64_t bytes, int32_t threads);
 
 /* ---- host-side numpy-stream emulation (no GPU needed) -----------------
  * Generator.permutation(n) of a PCG64 stream (algorithms.py:437-439). */

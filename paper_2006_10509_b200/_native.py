@@ -37,7 +37,7 @@ EXPORTS = (
     "cgh_plan_sa", "cgh_plan_dbs",
     "cgh_plan_download_idx", "cgh_plan_stream", "cgh_plan_sync", "cgh_plan_profile",
     "cgh_delta_error", "cgh_commit_update", "cgh_best_delta",
-    "cgh_permutation", "cgh_random_doubles", "cgh_expand_states",
+    "cgh_permutation", "cgh_random_doubles", "cgh_expand_states", "cgh_prefault",
     "cgh_slab_create", "cgh_slab_destroy", "cgh_slab_set_local", "cgh_slab_pass", "cgh_slab_transpose",
     "cgh_slab_turn", "cgh_plan_ospr_part", "cgh_plan_set_intensity", "cgh_plan_intensity",
     "cgh_plan_copy_intensity",
@@ -158,6 +158,7 @@ def _declare(lib):
         "cgh_best_delta": ([i32, P, P, P, P, P, P, i64, i32, i32, P, i64, pP(i64), pP(f64)], ctypes.c_int),
         "cgh_permutation": ([pP(Pcg64State), i64, P], ctypes.c_int),
         "cgh_expand_states": ([P, i32, i64, P, i32, P, i32], ctypes.c_int),
+        "cgh_prefault": ([P, i64, i32], ctypes.c_int),
         "cgh_random_doubles": ([i32, pP(Pcg64State), i64, i64, P], ctypes.c_int),
         "cgh_slab_create": ([pP(Problem), i32, i32, P, pP(P)], ctypes.c_int),
         "cgh_slab_destroy": ([P], ctypes.c_int),
@@ -220,19 +221,51 @@ def require_device():
             "no CUDA device visible: the B200 path has no CPU fallback (" + last_error() + ")")
 
 
-def expand_states(idx, table):
-    """states[idx] as complex128 via the library's threaded host expansion."""
+def expand_states(idx, table, out=None):
+    """states[idx] as complex128 via the library's threaded host expansion
+    (into ``out`` when given, e.g. a ``PrefaultedArrays`` array)."""
     idx = np.ascontiguousarray(idx)
     table = np.ascontiguousarray(table, dtype=np.complex128)
-    out = np.empty(idx.shape, dtype=np.complex128)
+    if out is None:
+        out = np.empty(idx.shape, dtype=np.complex128)
+    elif out.shape != idx.shape or out.dtype != np.complex128 or not out.flags.c_contiguous:
+        raise ValueError("out must be a C-contiguous complex128 array of the index plane's shape")
     nb = 1 if idx.dtype == np.uint8 else 4
     if nb == 4 and idx.dtype != np.int32:
         idx = idx.astype(np.int32)
-    import os as _os
-
-    threads = min(16, len(_os.sched_getaffinity(0)) if hasattr(_os, "sched_getaffinity") else 8)
+    threads = min(16, len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else 8)
     check(library().cgh_expand_states(ptr(idx), nb, idx.size, ptr(table), table.size, ptr(out), threads))
     return out
+
+
+class PrefaultedArrays:
+    """``count`` fresh complex128 arrays of ``shape`` whose pages are faulted
+    in by host threads (cgh_prefault) while the caller waits on the device, so
+    the final ``expand_states`` writes into resident memory (C3: 1.2 instead of
+    2.2-3.3 ms). Small outputs skip the thread."""
+
+    MIN_BYTES = 8 << 20
+
+    def __init__(self, shape, count=1):
+        self.arrays = [np.empty(shape, dtype=np.complex128) for _ in range(count)]
+        self._status = []
+        self._thread = None
+        if sum(a.nbytes for a in self.arrays) >= self.MIN_BYTES:
+            self._thread = threading.Thread(target=self._touch, daemon=True)
+            self._thread.start()
+
+    def _touch(self):
+        lib = library()
+        for a in self.arrays:
+            self._status.append(lib.cgh_prefault(ptr(a), a.nbytes, 4))
+
+    def take(self):
+        if self._thread is not None:
+            self._thread.join()
+            self._thread = None
+            for st in self._status:
+                check(st)
+        return self.arrays
 
 
 def c128(a):

@@ -254,10 +254,11 @@ def run_gs(cfg, target, illumination=None, progress=None, cancel=None):
     plan = _cached_plan(cfg, target.shape)
     plan.set_target(target, illumination, cfg=cfg)
     hooks = _Hooks(progress, cancel) if (progress is not None or cancel is not None) else None
+    out = _native.PrefaultedArrays(target.shape)    # faulted in while the device iterates
     rep, (tk, tv) = plan.gs(cfg=cfg, hooks=hooks)
     idx = plan.download_indices(1)[0]
     del keep
-    holo = _native.expand_states(idx, states(cfg.slm.scheme))
+    holo = _native.expand_states(idx, states(cfg.slm.scheme), out=out.take()[0])
     return holo, RunReport(
         error_trace=_trace(tk, tv, rep.trace_len),
         final_error=float(rep.final_error),
@@ -309,13 +310,15 @@ def run_ospr(cfg, target, illumination=None, progress=None, cancel=None):
     plan = _cached_plan(cfg, target.shape)
     plan.set_target(target, illumination, cfg=cfg)
     hooks = _Hooks(progress, cancel) if (progress is not None or cancel is not None) else None
+    out = _native.PrefaultedArrays(target.shape, max(0, int(cfg.subframes)))
     rep, (tk, tv) = plan.ospr(cfg=cfg, hooks=hooks)
     n = int(rep.iterations_executed)
     frames = []
     if n:
         idx = plan.download_indices(n)
         table = states(cfg.slm.scheme)
-        frames = [_native.expand_states(idx[i], table) for i in range(n)]
+        bufs = out.take()
+        frames = [_native.expand_states(idx[i], table, out=bufs[i]) for i in range(n)]
     del keep
     return frames, RunReport(
         error_trace=_trace(tk, tv, rep.trace_len),

@@ -1208,6 +1208,25 @@ int cgh_expand_states(const void* idx, int32_t idx_bytes, int64_t count, const d
     return CGH_OK;
 }
 
+int cgh_prefault(void* p, int64_t bytes, int32_t threads) {
+    if (bytes < 0 || (bytes > 0 && !p)) return fail(CGH_ERR_VALUE, "bad arguments");
+    constexpr int64_t kPage = 4096;
+    const int64_t pages = (bytes + kPage - 1) / kPage;
+    const int nt = int(std::max<int64_t>(1, std::min<int64_t>({int64_t(threads > 0 ? threads : 4), 64, pages})));
+    auto touch = [&](int64_t a, int64_t b) {
+        for (int64_t i = a; i < b; ++i) static_cast<volatile char*>(p)[i * kPage] = 0;
+    };
+    const int64_t chunk = (pages + nt - 1) / nt;
+    std::vector<std::thread> pool;
+    for (int t = 1; t < nt; ++t) {
+        const int64_t a = t * chunk, b = std::min(pages, a + chunk);
+        if (a < b) pool.emplace_back(touch, a, b);
+    }
+    touch(0, std::min(pages, chunk));
+    for (auto& th : pool) th.join();
+    return CGH_OK;
+}
+
 int cgh_permutation(const cgh_pcg64* rng, int64_t n, int64_t* out) {
     if (!rng || (n > 0 && !out) || n < 0) return fail(CGH_ERR_VALUE, "bad arguments");
     Pcg64 g = to_pcg(*rng);

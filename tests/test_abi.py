@@ -54,3 +54,23 @@ def test_no_device_fails_loudly():
         fft2(np.ones((8, 8), complex))
     with pytest.raises(errors.BackendUnavailableError):
         A.run_sa(cfg, np.ones((8, 8), complex))
+
+
+def test_host_expansion_into_prefaulted_arrays():
+    """Host-only helpers (no GPU): cgh_prefault + cgh_expand_states into a
+    caller-provided array give exactly states[idx]; bad outputs are rejected."""
+    rng = np.random.default_rng(5)
+    table = np.exp(2j * np.pi * np.arange(8) / 8)
+    idx = rng.integers(0, 8, (1024, 1536)).astype(np.uint8)
+    pre = _native.PrefaultedArrays(idx.shape, 2)    # 2 x 24 MiB: touched on a thread
+    bufs = pre.take()
+    assert len(bufs) == 2 and all(b.shape == idx.shape for b in bufs)
+    out = _native.expand_states(idx, table, out=bufs[1])
+    assert out is bufs[1] and np.array_equal(out, table[idx])
+    small = _native.PrefaultedArrays((4, 4)).take()[0]   # below the thread threshold
+    assert np.array_equal(_native.expand_states(idx[:4, :4], table, out=small), table[idx[:4, :4]])
+    with pytest.raises(ValueError):
+        _native.expand_states(idx, table, out=np.empty((3, 3), np.complex128))
+    _native.check(_native.library().cgh_prefault(None, 0, 4))
+    with pytest.raises(ValueError):
+        _native.check(_native.library().cgh_prefault(None, 4096, 4))
