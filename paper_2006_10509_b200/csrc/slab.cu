@@ -276,7 +276,8 @@ int cgh_slab_turn(cgh_slab* slab, const void* src, void* const* dst_blocks) {
     if (slab->G > kMaxTurnBlocks) return fail(CGH_ERR_UNSUPPORTED, "at most %d ranks", kMaxTurnBlocks);
     CGH_CUDA(cudaSetDevice(slab->dev));
     const int S = slab->R;
-    dim3 grid((S + 31) / 32, (S + 31) / 32, slab->G), block(32, 8);
+    const int TL = slab->prec == CGH_FP64 ? turn_tile<double>() : turn_tile<float>();
+    dim3 grid((S + TL - 1) / TL, (S + TL - 1) / TL, slab->G), block(32, 8);
     for (int g = 0; g < slab->G; ++g) {
         if (!dst_blocks[g]) return fail(CGH_ERR_VALUE, "null destination block %d", g);
         if (dst_blocks[g] == src) return fail(CGH_ERR_VALUE, "turn destination aliases the source");

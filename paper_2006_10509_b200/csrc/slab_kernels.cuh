@@ -302,30 +302,42 @@ __global__ void __launch_bounds__(256) slab_transpose_kernel(const cx<T>* __rest
 // Corner turn fused with the exchange: block g of the local slab is
 // transposed through shared memory and stored straight into dst.p[g] (another
 // rank's receive buffer over NVLink peer mappings, another virtual rank's
-// buffer, or the local buffer when G = 1), 32 x 32 tiles, 256-B coalesced
-// rows on both sides.
+// buffer, or the local buffer when G = 1).
 constexpr int kMaxTurnBlocks = 64;
 template <class T>
 struct TurnTargets {
     cx<T>* p[kMaxTurnBlocks];
 };
 
+// TL x TL tiles (64 for complex64: 512-B row segments on both sides, which
+// keeps DRAM pages open longer than 32-wide tiles; 32 for complex128 to stay
+// within static shared memory), 256 threads.
+template <class T>
+constexpr int turn_tile() { return sizeof(T) == 4 ? 64 : 32; }
+
 template <class T>
 __global__ void __launch_bounds__(256) slab_turn_kernel(const cx<T>* __restrict__ src, TurnTargets<T> dst, int S) {
-    __shared__ cx<T> tile[32][33];
+    constexpr int TL = turn_tile<T>();
+    __shared__ cx<T> tile[TL][TL + 1];
     const int g = blockIdx.z;
     const cx<T>* s = src + long(g) * S * S;
     cx<T>* d = dst.p[g];
-    const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 32;
-    for (int k = threadIdx.y; k < 32; k += 8) {
-        const int y = y0 + k, x = x0 + threadIdx.x;
-        if (y < S && x < S) tile[k][threadIdx.x] = s[long(y) * S + x];
-    }
+    const int x0 = blockIdx.x * TL, y0 = blockIdx.y * TL;
+#pragma unroll
+    for (int k = threadIdx.y; k < TL; k += 8)
+#pragma unroll
+        for (int c = 0; c < TL; c += 32) {
+            const int y = y0 + k, x = x0 + c + threadIdx.x;
+            if (y < S && x < S) tile[k][c + threadIdx.x] = s[long(y) * S + x];
+        }
     __syncthreads();
-    for (int k = threadIdx.y; k < 32; k += 8) {
-        const int y = x0 + k, x = y0 + threadIdx.x;
-        if (y < S && x < S) d[long(y) * S + x] = tile[threadIdx.x][k];
-    }
+#pragma unroll
+    for (int k = threadIdx.y; k < TL; k += 8)
+#pragma unroll
+        for (int c = 0; c < TL; c += 32) {
+            const int y = x0 + k, x = y0 + c + threadIdx.x;
+            if (y < S && x < S) d[long(y) * S + x] = tile[c + threadIdx.x][k];
+        }
 }
 
 template <class T, int N, int MODE>
