@@ -40,8 +40,12 @@ __global__ void prep_kernel(const double* __restrict__ tc, const uint8_t* __rest
     const long total = long(H) * W;
     double cnt = 0, den = 0, nfm = 0, nfa = 0, nfb = 0;
     for (long p = long(blockIdx.x) * blockDim.x + threadIdx.x; p < total; p += long(gridDim.x) * blockDim.x) {
-        const int u = int(p / W), v = int(p - long(u) * W);
-        const int uc = (u + H / 2) % H, vc = (v + W / 2) % W;
+        // planes are < 2^31 pixels (cgh_plan_create): 32-bit division, no modulo
+        const unsigned pu = unsigned(p), uu = pu / unsigned(W);
+        const int u = int(uu), v = int(pu - uu * unsigned(W));
+        int uc = u + H / 2, vc = v + W / 2;
+        if (uc >= H) uc -= H;
+        if (vc >= W) vc -= W;
         const long pc = long(uc) * W + vc;
         const double re = tc[2 * pc], im = tc[2 * pc + 1];
         const double t = hypot(re, im);
@@ -83,14 +87,33 @@ __global__ void prep_kernel(const double* __restrict__ tc, const uint8_t* __rest
         last = atomicAdd(ps.counter, 1u) == gridDim.x - 1;
     }
     __syncthreads();
-    if (last && threadIdx.x == 0) {
+    if (last) {
+        // the whole last block sums the partials (strided per thread, then a
+        // fixed shuffle/warp tree: deterministic); one thread summing up to
+        // 2368 x 5 partials serially took most of the kernel's time
         __threadfence();
+        double tot[5];
+#pragma unroll
         for (int q = 0; q < 5; ++q) {
             double s = 0;
-            for (unsigned b = 0; b < gridDim.x; ++b) s += __ldcg(&ps.partials[q * gridDim.x + b]);
-            ps.out[q] = s;
+            for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x) s += __ldcg(&ps.partials[q * gridDim.x + b]);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+            tot[q] = s;
         }
-        *ps.counter = 0u;
+        __syncthreads();
+        if (lane == 0)
+#pragma unroll
+            for (int q = 0; q < 5; ++q) sh[q * 32 + warp] = tot[q];
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int q = 0; q < 5; ++q) {
+                double s = 0;
+                for (int w = 0; w < nw; ++w) s += sh[q * 32 + w];
+                ps.out[q] = s;
+            }
+            *ps.counter = 0u;
+        }
     }
 }
 

@@ -862,14 +862,30 @@ __global__ void masked_sums_kernel(const double* __restrict__ rep, const double*
         last = atomicAdd(counter, 1u) == gridDim.x - 1;
     }
     __syncthreads();
-    if (last && threadIdx.x == 0) {
+    if (last) {   // whole last block, fixed order (see prep_kernel)
         __threadfence();
+        double tot[6];
+#pragma unroll
         for (int q = 0; q < 6; ++q) {
             double s = 0;
-            for (unsigned b = 0; b < gridDim.x; ++b) s += __ldcg(&partials[q * gridDim.x + b]);
-            out[q] = s;
+            for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x) s += __ldcg(&partials[q * gridDim.x + b]);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+            tot[q] = s;
         }
-        *counter = 0u;
+        __syncthreads();
+        if (lane == 0)
+#pragma unroll
+            for (int q = 0; q < 6; ++q) sh[q * 32 + warp] = tot[q];
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int q = 0; q < 6; ++q) {
+                double s = 0;
+                for (int w = 0; w < nw; ++w) s += sh[q * 32 + w];
+                out[q] = s;
+            }
+            *counter = 0u;
+        }
     }
 }
 
