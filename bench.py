@@ -436,6 +436,13 @@ def run_ours(args):
                 exch_kind = "fused turn kernel: transposed blocks stored to peer buffers over NVLink + device barrier"
             except Exception as exc:  # noqa: BLE001
                 exch_kind = f"nccl all_to_all_single (symmetric memory unavailable: {type(exc).__name__}: {exc})"
+            if world > 1:   # every rank takes the same exchange
+                ok = torch.tensor([1 if sess is not None else 0], dtype=torch.int32, device=f"cuda:{local}")
+                dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+                if int(ok.item()) == 0 and sess is not None:
+                    sess.close()
+                    sess = None
+                    exch_kind = "nccl all_to_all_single (symmetric memory unavailable on another rank)"
         if sess is None:
             sess = SL.SlabSession(c6cfg, target6, exchange=SL.TorchExchange() if world > 1 else None,
                                   precision=_native.FP32, device=local)
