@@ -145,7 +145,9 @@ int cgh_device_count(int32_t *count);
 
 /* ---- transforms: propagation.py:81-94 (fft2), 110-123 (propagate[_inverse])
  * op 0 = fft2 forward (centred), 1 = fft2 inverse, 2 = propagate,
- * 3 = propagate_inverse. in/out: H*W complex128. Sizes: powers of two. */
+ * 3 = propagate_inverse. in/out: H*W complex128. Power-of-two sides up to 4096
+ * run the row/column passes; any other shape runs Bluestein line transforms
+ * (sides up to 4096 in fp64, 8192 in fp32). */
 int cgh_transform(const cgh_problem *pb, const double *in, double *out, int32_t op);
 
 /* ---- masked metric sums on the device, fp64, fixed order (mse_error /

@@ -145,7 +145,7 @@ __global__ void store_field_kernel(const cx<T>* __restrict__ in, double* __restr
     for (long p = long(blockIdx.x) * blockDim.x + threadIdx.x; p < total; p += long(gridDim.x) * blockDim.x) {
         const int u = int(p / W), v = int(p - long(u) * W);
         long dst = p;
-        if (shift) dst = long((u + H - H / 2) % H) * W + (v + W - W / 2) % W;
+        if (shift) dst = long((u + H / 2) % H) * W + (v + W / 2) % W;   // np.fft.fftshift, odd sides too
         cx<T> z = in[p];
         if (qr) z = cmulc(z, cmul(qr[u], qc[v]));
         out[2 * dst] = double(z.x);

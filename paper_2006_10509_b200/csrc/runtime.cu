@@ -1063,8 +1063,15 @@ struct PlanGuard {
 };
 
 int cgh_transform(const cgh_problem* pb, const double* in, double* out, int32_t op) {
-    if (!in || !out) return fail(CGH_ERR_VALUE, "null buffer");
+    if (!in || !out || !pb) return fail(CGH_ERR_VALUE, "null buffer");
     if (op < 0 || op > 3) return fail(CGH_ERR_VALUE, "direction must be 'forward' or 'inverse'");
+    if (pb->height >= 1 && pb->width >= 1 &&
+        (!is_pow2(pb->height) || !is_pow2(pb->width) || pb->height > (1 << kMaxLog2) || pb->width > (1 << kMaxLog2))) {
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(CGH_ERR_NO_DEVICE, "no CUDA device");
+        if (pb->device < 0 || pb->device >= ndev) return fail(CGH_ERR_VALUE, "device %d out of range", pb->device);
+        return transform_any(pb, in, out, op);   // Bluestein line transforms (anysize.cu)
+    }
     PlanGuard g;
     CGH_TRY(cgh_plan_create(pb, &g.p));
     return g.p->prec == CGH_FP64 ? transform_exec<double>(g.p, in, out, op) : transform_exec<float>(g.p, in, out, op);

@@ -92,6 +92,8 @@ namespace cgh {
 
 // fp64 tables (long-double evaluation): exp(-2 pi i k / n); separable Fresnel chirp
 void twiddle_table(int n, std::vector<double>& out);
+// centred transform of any H x W (anysize.cu; Bluestein line DFTs)
+int transform_any(const cgh_problem* pb, const double* in, double* out, int op);
 void chirp_table(int n, double pitch, double wl, double dist, std::vector<double>& out);
 
 int plan_init(cgh_plan* P, const cgh_problem* pb);
