@@ -123,7 +123,7 @@ static cudaError_t blue_launch(int M, const BlueArgs<T>& a, int sms, cudaStream_
     }
 }
 
-static int blue_length(int n) {
+int blue_length(int n) {
     int m = 64;
     while (m < 2 * n - 1) m *= 2;
     return m;
@@ -297,6 +297,298 @@ static int any_transform(const cgh_problem* pb, const double* in, double* out, i
     CGH_CUDA(cudaGetLastError());
     CGH_CUDA(cudaMemcpyAsync(out, stage, size_t(n) * 16, cudaMemcpyDeviceToHost, B.st));
     CGH_CUDA(cudaStreamSynchronize(B.st));
+    return CGH_OK;
+}
+
+// ====================================================== GS passes, any N
+// The row/column pass modes of pass_kernels.cuh for a line length N that is
+// not a power of two: the line DFTs are Bluestein transforms on M-point line
+// FFTs, the per-pixel work (random-phase start, hologram projection and
+// snapping, replay projection, error sums) is the same code as the
+// power-of-two passes. Element j of the line sits at v[r], j = t + r * TF
+// (TF = M / E threads), entries j >= N are zero.
+
+template <class T, int M, int E>
+__device__ __forceinline__ void blue_dft(cx<T> (&v)[E], int dir, int N, T* sre, T* sim, int t, const cx<T>* tab) {
+    constexpr int TF = M / E;
+    const cx<T>* chirp = tab;
+    const cx<T>* filt = tab + N;
+    const cx<T>* twm = tab + N + M;
+#pragma unroll
+    for (int r = 0; r < E; ++r) {
+        const int j = t + r * TF;
+        v[r] = j < N ? (dir < 0 ? cmul(v[r], chirp[j]) : cmulc(v[r], chirp[j])) : mk<T>(0, 0);
+    }
+    LineFft<T, M, -1, E>::run(v, sre, sim, t, twm);
+#pragma unroll
+    for (int r = 0; r < E; ++r) v[r] = dir < 0 ? cmul(v[r], filt[t + r * TF]) : cmulc(v[r], filt[t + r * TF]);
+    LineFft<T, M, +1, E>::run(v, sre, sim, t, twm);
+    const T inv = T(1) / T(M);
+#pragma unroll
+    for (int r = 0; r < E; ++r) {
+        const int j = t + r * TF;
+        v[r] = j < N ? (dir < 0 ? cmul(v[r], chirp[j]) : cmulc(v[r], chirp[j])) * inv : mk<T>(0, 0);
+    }
+}
+
+template <class T, int M>
+struct AnyShape {
+    static constexpr int E = LineShape<T, M>::E;
+    static constexpr int TF = M / E;
+    static constexpr size_t FFT_BYTES = size_t(2) * line_words<T, M>() * sizeof(T);
+    static constexpr size_t SMEM = ((FFT_BYTES + 15) & ~size_t(15)) + kRedWords * sizeof(double);
+};
+
+template <class T, int M, int MODE>
+__global__ void __launch_bounds__(AnyShape<T, M>::TF) any_row_kernel(PassArgs<T> a) {
+    using Sh = AnyShape<T, M>;
+    constexpr int E = Sh::E, TF = Sh::TF;
+    extern __shared__ __align__(16) unsigned char smem[];
+    T* sre = reinterpret_cast<T*>(smem);
+    T* sim = sre + line_words<T, M>();
+    const int t = threadIdx.x, m = blockIdx.x, N = a.W;
+    cx<T>* row = a.data + long(blockIdx.y) * a.frame_stride + long(m) * N;
+    cx<T> v[E];
+    if constexpr (MODE == ROW_INIT) {
+        // contiguous chunks of the row-major draws per thread, staged in smem
+        const int ch = (N + TF - 1) / TF, j0 = t * ch, j1 = min(N, j0 + ch);
+        if (j0 < j1) {
+            Pcg64 g = a.rng;
+            pcg_advance(g, uint64_t(long(m) * N + j0));
+            for (int j = j0; j < j1; ++j) {
+                const cx<T> z = unit_phase<T>(g);
+                const T amp = a.beam ? a.beam[long(m) * N + j] : T(1);
+                sre[padx<T>(j)] = amp * z.x;
+                sim[padx<T>(j)] = amp * z.y;
+            }
+        }
+        __syncthreads();
+        const bool fres = a.q_row != nullptr;
+#pragma unroll
+        for (int r = 0; r < E; ++r) {
+            const int n = t + r * TF;
+            if (n < N) {
+                cx<T> h = mk(sre[padx<T>(n)], sim[padx<T>(n)]);
+                if (a.field_out) a.field_out[long(m) * N + n] = h;
+                if (a.quantize) {
+                    const int k = quantize_index<T>(a.scheme, h);
+                    if (a.idx_out) {
+                        const long p = long(m) * N + n;
+                        if (a.idx_bytes == 1) static_cast<uint8_t*>(a.idx_out)[p] = (uint8_t)k;
+                        else static_cast<int32_t*>(a.idx_out)[p] = k;
+                    }
+                    h = state_value<T>(a.scheme, k);
+                }
+                if (fres) h = cmul(h, cmul(a.q_row[m], a.q_col[n]));
+                v[r] = h;
+            } else {
+                v[r] = mk<T>(0, 0);
+            }
+        }
+        blue_dft<T, M, E>(v, -1, N, sre, sim, t, a.tw_row);
+    } else {   // ROW_FWD, ROW_INV, ROW_HOLO
+#pragma unroll
+        for (int r = 0; r < E; ++r) v[r] = t + r * TF < N ? row[t + r * TF] : mk<T>(0, 0);
+        blue_dft<T, M, E>(v, MODE == ROW_FWD ? -1 : +1, N, sre, sim, t, a.tw_row);
+        if constexpr (MODE == ROW_HOLO) {
+#pragma unroll
+            for (int r = 0; r < E; ++r)
+                if (t + r * TF < N) v[r] = holo_project<T>(a, v[r], m, t + r * TF, 0);
+            blue_dft<T, M, E>(v, -1, N, sre, sim, t, a.tw_row);
+        } else if (a.scale != T(1)) {
+#pragma unroll
+            for (int r = 0; r < E; ++r) v[r] = v[r] * a.scale;
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < E; ++r)
+        if (t + r * TF < N) row[t + r * TF] = v[r];
+}
+
+template <class T, int M, int MODE>
+__global__ void __launch_bounds__(AnyShape<T, M>::TF) any_col_kernel(PassArgs<T> a) {
+    using Sh = AnyShape<T, M>;
+    constexpr int E = Sh::E, TF = Sh::TF;
+    extern __shared__ __align__(16) unsigned char smem[];
+    T* sre = reinterpret_cast<T*>(smem);
+    T* sim = sre + line_words<T, M>();
+    double* rs = red_scratch<T>(smem, Sh::FFT_BYTES);
+    const int t = threadIdx.x, n = blockIdx.x, N = a.H;
+    const long W = a.W;
+    cx<T>* col = a.data + long(blockIdx.y) * a.frame_stride + n;
+    cx<T> v[E];
+#pragma unroll
+    for (int r = 0; r < E; ++r) v[r] = t + r * TF < N ? col[long(t + r * TF) * W] : mk<T>(0, 0);
+    if constexpr (MODE == COL_FWD || MODE == COL_INV) {
+        blue_dft<T, M, E>(v, MODE == COL_FWD ? -1 : +1, N, sre, sim, t, a.tw_col);
+        if (a.scale != T(1)) {
+#pragma unroll
+            for (int r = 0; r < E; ++r) v[r] = v[r] * a.scale;
+        }
+    } else {   // COL_GS, COL_FINAL (col_kernel's epilogue)
+        blue_dft<T, M, E>(v, -1, N, sre, sim, t, a.tw_col);
+        T sdd = 0, srr = 0, srd = 0, sall = 0;
+        const T gain = a.gain;
+#pragma unroll
+        for (int r = 0; r < E; ++r) {
+            const int u = t + r * TF;
+            if (u >= N) continue;
+            const cx<T> R = v[r] * a.scale;
+            const T r2 = R.x * R.x + R.y * R.y;
+            const T rr = dev_sqrt<T>(r2);
+            const T tt = a.tgt[long(u) * W + n];
+            sall += r2;
+            cx<T> out = R;
+            if (!signbit(tt)) {
+                const T d = rr - tt;
+                sdd += d * d;
+                srr += r2;
+                srd += rr * d;
+                if constexpr (MODE == COL_GS) {
+                    T want = tt + gain * (tt - rr);
+                    want = want > T(0) ? want : T(0);
+                    if (rr > T(0)) {
+                        const T s = want / rr;
+                        out = mk(R.x * s, R.y * s);
+                    } else {
+                        out = mk(want, T(0));
+                    }
+                }
+            }
+            v[r] = out;
+        }
+        if constexpr (MODE == COL_GS) blue_dft<T, M, E>(v, +1, N, sre, sim, t, a.tw_col);
+        double acc[4] = {double(sdd), double(srr), double(srd), double(sall)};
+        block_reduce<4>(acc, rs);
+        const int nblocks = gridDim.x;
+        if (publish_partials<4>(a.red, acc, nblocks, blockIdx.x)) {
+            const double s_dd = sum_partials(a.red, 0, nblocks, rs);
+            const double s_rr = sum_partials(a.red, 1, nblocks, rs);
+            const double s_rd = sum_partials(a.red, 2, nblocks, rs);
+            const double s_all = sum_partials(a.red, 3, nblocks, rs);
+            if (threadIdx.x == 0) {
+                a.red.out[0] = error_from_sums(s_dd, s_rr, s_rd, *a.red.denom, a.red.rescale);
+                a.red.out[1] = s_all == 0.0 ? __longlong_as_double(0x7ff8000000000000LL) : s_rr / s_all;
+                *a.red.counter = 0u;
+            }
+        }
+        if constexpr (MODE == COL_FINAL) return;
+    }
+#pragma unroll
+    for (int r = 0; r < E; ++r)
+        if (t + r * TF < N) col[long(t + r * TF) * W] = v[r];
+}
+
+template <class T, int M, class K>
+static cudaError_t any_launch(K kernel, int lines, int frames, cudaStream_t st, const PassArgs<T>& a) {
+    using Sh = AnyShape<T, M>;
+    if (Sh::SMEM > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(Sh::SMEM));
+        if (e != cudaSuccess) return e;
+    }
+    kernel<<<dim3(lines, frames), Sh::TF, Sh::SMEM, st>>>(a);
+    return cudaGetLastError();
+}
+
+template <class T, int M>
+static cudaError_t any_row_m(int mode, const PassArgs<T>& a, int frames, cudaStream_t st) {
+    switch (mode) {
+        case ROW_FWD: return any_launch<T, M>(any_row_kernel<T, M, ROW_FWD>, a.H, frames, st, a);
+        case ROW_INV: return any_launch<T, M>(any_row_kernel<T, M, ROW_INV>, a.H, frames, st, a);
+        case ROW_HOLO: return any_launch<T, M>(any_row_kernel<T, M, ROW_HOLO>, a.H, frames, st, a);
+        case ROW_INIT: return any_launch<T, M>(any_row_kernel<T, M, ROW_INIT>, a.H, frames, st, a);
+        default: return cudaErrorNotSupported;   // OSPR passes: power-of-two planes only
+    }
+}
+
+template <class T, int M>
+static cudaError_t any_col_m(int mode, const PassArgs<T>& a, int frames, cudaStream_t st) {
+    switch (mode) {
+        case COL_FWD: return any_launch<T, M>(any_col_kernel<T, M, COL_FWD>, a.W, frames, st, a);
+        case COL_INV: return any_launch<T, M>(any_col_kernel<T, M, COL_INV>, a.W, frames, st, a);
+        case COL_GS: return any_launch<T, M>(any_col_kernel<T, M, COL_GS>, a.W, frames, st, a);
+        case COL_FINAL: return any_launch<T, M>(any_col_kernel<T, M, COL_FINAL>, a.W, frames, st, a);
+        default: return cudaErrorNotSupported;
+    }
+}
+
+#define CGH_ANY_SIZES(X) X(64) X(128) X(256) X(512) X(1024) X(2048) X(4096) X(8192)
+
+template <class T>
+cudaError_t launch_row_any(int mode, int N, const PassArgs<T>& a, int frames, cudaStream_t st) {
+    if (N < 1 || N > kMaxAnyLine) return cudaErrorInvalidValue;
+#define CGH_ANY_ROW(MM) case MM: return any_row_m<T, MM>(mode, a, frames, st);
+    switch (blue_length(N)) {
+        CGH_ANY_SIZES(CGH_ANY_ROW)
+        default: return cudaErrorInvalidValue;
+    }
+#undef CGH_ANY_ROW
+}
+
+template <class T>
+cudaError_t launch_col_any(int mode, int N, const PassArgs<T>& a, int frames, cudaStream_t st) {
+    if (N < 1 || N > kMaxAnyLine) return cudaErrorInvalidValue;
+#define CGH_ANY_COL(MM) case MM: return any_col_m<T, MM>(mode, a, frames, st);
+    switch (blue_length(N)) {
+        CGH_ANY_SIZES(CGH_ANY_COL)
+        default: return cudaErrorInvalidValue;
+    }
+#undef CGH_ANY_COL
+}
+
+template cudaError_t launch_row_any<float>(int, int, const PassArgs<float>&, int, cudaStream_t);
+template cudaError_t launch_row_any<double>(int, int, const PassArgs<double>&, int, cudaStream_t);
+template cudaError_t launch_col_any<float>(int, int, const PassArgs<float>&, int, cudaStream_t);
+template cudaError_t launch_col_any<double>(int, int, const PassArgs<double>&, int, cudaStream_t);
+
+// Packed Bluestein table of a plan axis of length N (host part): chirp [N],
+// convolution kernel b [M] (its spectrum is taken on the device by
+// blue_finish_table), twiddles exp(-2 pi i k / M) [M].
+void blue_pack_table(int N, std::vector<double>& out) {
+    const int M = blue_length(N);
+    std::vector<double> chirp, b, tw;
+    chirp_tables(N, M, chirp, b);
+    twiddle_table(M, tw);
+    out.clear();
+    out.insert(out.end(), chirp.begin(), chirp.end());
+    out.insert(out.end(), b.begin(), b.end());
+    out.insert(out.end(), tw.begin(), tw.end());
+}
+
+int blue_finish_table(int prec, int N, void* dev_table, cudaStream_t st) {
+    const int M = blue_length(N);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaError_t e;
+    if (prec == CGH_FP64) {
+        cx<double>* t = static_cast<cx<double>*>(dev_table);
+        BlueArgs<double> a{};
+        a.data = t + N;
+        a.N = M;
+        a.lines = 1;
+        a.line_stride = M;
+        a.elem_stride = 1;
+        a.tw = t + N + M;
+        a.dir = -1;
+        a.scale = 1.0;
+        a.plain = 1;
+        e = blue_launch<double>(M, a, sms, st);
+    } else {
+        cx<float>* t = static_cast<cx<float>*>(dev_table);
+        BlueArgs<float> a{};
+        a.data = t + N;
+        a.N = M;
+        a.lines = 1;
+        a.line_stride = M;
+        a.elem_stride = 1;
+        a.tw = t + N + M;
+        a.dir = -1;
+        a.scale = 1.0f;
+        a.plain = 1;
+        e = blue_launch<float>(M, a, sms, st);
+    }
+    if (e != cudaSuccess) return fail(CGH_ERR_CUDA, "Bluestein table (N=%d): %s", N, cudaGetErrorString(e));
     return CGH_OK;
 }
 

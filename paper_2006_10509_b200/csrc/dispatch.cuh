@@ -22,6 +22,17 @@ int row_grid_blocks(int N, int H);
 template <class T>
 int col_grid_blocks(int N, int W);
 
+// Non-power-of-two line lengths (anysize.cu): the same row/column pass modes
+// with Bluestein line DFTs; one CTA per line. The line's twiddle table
+// (PassArgs tw_row / tw_col) is then the packed Bluestein table of
+// blue_pack_table: chirp [N] | chirp-filter spectrum [M] | exp(-2 pi i k / M) [M].
+template <class T>
+cudaError_t launch_row_any(int mode, int N, const PassArgs<T>& a, int frames, cudaStream_t st);
+template <class T>
+cudaError_t launch_col_any(int mode, int N, const PassArgs<T>& a, int frames, cudaStream_t st);
+int blue_length(int n);
+constexpr int kMaxAnyLine = 4096;   // non-power-of-two sides of GS plans
+
 // ---------------------------------------------------------------- prep
 // Build the uncentred (ifftshifted) target amplitude with the mask folded in
 // as the sign bit, the hologram-plane beam amplitude, and optionally the

@@ -15,7 +15,7 @@ template <>
 cudaError_t launch_row<CGH_T>(int mode, int N, const PassArgs<CGH_T>& a, int frames, cudaStream_t st) {
     switch (N) {
         CGH_ALL_SIZES(CGH_ROW_CASE)
-        default: return cudaErrorInvalidValue;
+        default: return launch_row_any<CGH_T>(mode, N, a, frames, st);
     }
 }
 
@@ -23,7 +23,7 @@ template <>
 cudaError_t launch_col<CGH_T>(int mode, int N, const PassArgs<CGH_T>& a, int frames, cudaStream_t st) {
     switch (N) {
         CGH_ALL_SIZES(CGH_COL_CASE)
-        default: return cudaErrorInvalidValue;
+        default: return launch_col_any<CGH_T>(mode, N, a, frames, st);
     }
 }
 
@@ -31,14 +31,14 @@ template <>
 int row_grid_blocks<CGH_T>(int N, int H) {
     switch (N) {
         CGH_ALL_SIZES(CGH_RB_CASE)
-        default: return 0;
+        default: return H;   // Bluestein rows: one CTA per line
     }
 }
 template <>
 int col_grid_blocks<CGH_T>(int N, int W) {
     switch (N) {
         CGH_ALL_SIZES(CGH_CB_CASE)
-        default: return 0;
+        default: return W;   // Bluestein columns: one CTA per line
     }
 }
 

@@ -115,9 +115,10 @@ int plan_init(cgh_plan* P, const cgh_problem* pb) {
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(CGH_ERR_NO_DEVICE, "no CUDA device");
     if (pb->device < 0 || pb->device >= ndev) return fail(CGH_ERR_VALUE, "device %d out of range (%d devices)", pb->device, ndev);
     if (pb->height < 1 || pb->width < 1) return fail(CGH_ERR_DIMENSION, "empty shape %dx%d", pb->height, pb->width);
-    if (!is_pow2(pb->height) || !is_pow2(pb->width) || pb->height > (1 << kMaxLog2) || pb->width > (1 << kMaxLog2))
-        return fail(CGH_ERR_UNSUPPORTED, "shape %dx%d: the CUDA path implements power-of-two sides 2..%d",
-                    pb->height, pb->width, 1 << kMaxLog2);
+    // power-of-two sides run the radix-16 passes; other sides Bluestein line DFTs (anysize.cu)
+    if (pb->height < 2 || pb->width < 2 || pb->height > kMaxAnyLine || pb->width > kMaxAnyLine)
+        return fail(CGH_ERR_UNSUPPORTED, "shape %dx%d: the CUDA path implements sides 2..%d",
+                    pb->height, pb->width, kMaxAnyLine);
     if (pb->precision != CGH_FP32 && pb->precision != CGH_FP64) return fail(CGH_ERR_VALUE, "bad precision");
     if (pb->n_states < 2 || !pb->states) return fail(CGH_ERR_VALUE, "scheme needs >= 2 states");
     if (pb->prop_kind == CGH_FRESNEL) {
@@ -163,10 +164,22 @@ int plan_init(cgh_plan* P, const cgh_problem* pb) {
     CGH_CUDA(cudaMemcpyAsync(P->states32.p, s32.data(), ns * 8, cudaMemcpyHostToDevice, P->st));
     // tables
     std::vector<double> t;
-    twiddle_table(P->W, t);
-    CGH_TRY(upload_table(P, P->tw_row, t));
-    twiddle_table(P->H, t);
-    CGH_TRY(upload_table(P, P->tw_col, t));
+    if (is_pow2(P->W)) {
+        twiddle_table(P->W, t);
+        CGH_TRY(upload_table(P, P->tw_row, t));
+    } else {
+        blue_pack_table(P->W, t);
+        CGH_TRY(upload_table(P, P->tw_row, t));
+        CGH_TRY(blue_finish_table(P->prec, P->W, P->tw_row.p, P->st));
+    }
+    if (is_pow2(P->H)) {
+        twiddle_table(P->H, t);
+        CGH_TRY(upload_table(P, P->tw_col, t));
+    } else {
+        blue_pack_table(P->H, t);
+        CGH_TRY(upload_table(P, P->tw_col, t));
+        CGH_TRY(blue_finish_table(P->prec, P->H, P->tw_col.p, P->st));
+    }
     if (P->prop_kind == CGH_FRESNEL) {
         chirp_table(P->H, P->py, P->wl, P->dist, t);
         CGH_TRY(upload_table(P, P->q_row, t));
@@ -571,6 +584,8 @@ template <class T>
 static int ospr_exec(cgh_plan* P, const cgh_ospr_params* op, int64_t* tk, double* tv, int64_t cap, cgh_report* rep,
                      const cgh_callbacks* cb) {
     if (!P->target_ready) return fail(CGH_ERR_VALUE, "target not set");
+    if (!is_pow2(P->H) || !is_pow2(P->W))
+        return fail(CGH_ERR_UNSUPPORTED, "OSPR: power-of-two planes only (got %dx%d)", P->H, P->W);
     const int S = std::max(0, op->subframes);
     if (S > 0 && !op->frame_rng) return fail(CGH_ERR_VALUE, "frame streams missing");
     // reference order per frame: propagate_inverse(sub_target) -> ... -> mse_error
@@ -711,6 +726,8 @@ static int ospr_exec(cgh_plan* P, const cgh_ospr_params* op, int64_t* tk, double
 template <class T>
 static int ospr_part_exec(cgh_plan* P, const cgh_ospr_params* op, int frame0, int nframes_total, int phase,
                           int64_t* tk, double* tv, int64_t cap, cgh_report* rep) {
+    if (!is_pow2(P->H) || !is_pow2(P->W))
+        return fail(CGH_ERR_UNSUPPORTED, "OSPR: power-of-two planes only (got %dx%d)", P->H, P->W);
     if (!P->target_ready) return fail(CGH_ERR_VALUE, "target not set");
     const int m = std::max(0, op->subframes);
     if (m < 1 || m > 64) return fail(CGH_ERR_UNSUPPORTED, "a sharded OSPR part holds 1..64 subframes (got %d)", m);

@@ -94,6 +94,9 @@ namespace cgh {
 void twiddle_table(int n, std::vector<double>& out);
 // centred transform of any H x W (anysize.cu; Bluestein line DFTs)
 int transform_any(const cgh_problem* pb, const double* in, double* out, int op);
+// packed Bluestein tables of non-power-of-two plan axes (anysize.cu)
+void blue_pack_table(int N, std::vector<double>& out);
+int blue_finish_table(int prec, int N, void* dev_table, cudaStream_t st);
 void chirp_table(int n, double pitch, double wl, double dist, std::vector<double>& out);
 
 int plan_init(cgh_plan* P, const cgh_problem* pb);

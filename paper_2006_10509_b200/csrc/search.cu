@@ -628,6 +628,8 @@ static int search_alloc(SearchRun& S, size_t bytes, void** out) {
 // Initial index plane + uncentred replay + masked gather (algorithms.py:217-251).
 static int search_setup(SearchRun& S, int init_mode, const cgh_pcg64& rng0, bool dbs) {
     cgh_plan* P = S.P;
+    if (!is_pow2(P->H) || !is_pow2(P->W))   // the DFT table indexing uses power-of-two masks
+        return fail(CGH_ERR_UNSUPPORTED, "SA/DBS: power-of-two planes only (got %dx%d)", P->H, P->W);
     const long long n = (long long)P->H * P->W;
     CGH_TRY(ensure(P, P->data, size_t(n) * 16));
     CGH_TRY(ensure(P, P->idx, size_t(n) * P->idx_bytes));

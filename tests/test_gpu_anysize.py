@@ -72,3 +72,83 @@ def test_any_shape_errors_are_loud():
         P.fft2(h, "forward")
     with pytest.raises(UnsupportedShapeError):
         P.fft2(np.ones((5000, 6), complex), "forward")   # beyond the fp64 Bluestein lines
+
+
+# ---------------------------------------------------------------- GS runners
+from paper_2006_10509_b200 import algorithms as A  # noqa: E402
+from paper_2006_10509_b200.image import rect_mask  # noqa: E402
+from paper_2006_10509_b200.propagation import MetricSpec, PropagationSpec  # noqa: E402
+from paper_2006_10509_b200.runtime import precision  # noqa: E402
+from paper_2006_10509_b200.slm import PhaseOnly, SlmSpec, binary_phase  # noqa: E402
+from paper_2006_10509_b200.workloads import gaussian_beam  # noqa: E402
+
+
+def _target(h, w):
+    y, x = np.mgrid[0:h, 0:w]
+    return np.clip(0.3 + 0.5 * np.exp(-(((x - 0.4 * w) / (0.2 * w)) ** 2 + ((y - 0.6 * h) / (0.25 * h)) ** 2)),
+                   0, 1).astype(complex)
+
+
+def _cfg(h, w, kind="fourier", levels=8, mask=False, gain=0.0, init="random-phase", iters=10, qe=False):
+    rects = [(w // 5, h // 6, w // 2, h // 2)] if mask else []     # (x, y, w, h)
+    scheme = binary_phase() if levels == 2 else PhaseOnly(levels)
+    return A.AlgorithmConfig("gs", SlmSpec(w, h, scheme), PropagationSpec(kind, distance=0.05),
+                             MetricSpec(rect_mask(w, h, rects), rescale=mask), seed=4, iterations=iters,
+                             feedback_gain=gain, quantize_each_iteration=qe, init_mode=init)
+
+
+@pytest.mark.parametrize("h,w,kind,levels,mask,gain,init,beam,qe", [
+    (48, 80, "fourier", 8, False, 0.0, "random-phase", False, False),
+    (45, 60, "fresnel", 2, True, 0.3, "random-phase", True, False),
+    (33, 31, "fourier", 16, False, 0.0, "backpropagate", False, False),
+    (100, 64, "fresnel", 4, True, 0.0, "random-phase", False, True),     # non-power-of-two rows only
+    (64, 96, "fourier", 8, False, 0.2, "random-phase", False, False),    # non-power-of-two columns only
+])
+def test_gs_any_shape_fp64_matches_oracle(h, w, kind, levels, mask, gain, init, beam, qe):
+    """run_gs on planes the radix-16 passes do not take (Bluestein line DFTs):
+    fp64 traces within 1e-9 of the oracle (pocketfft rounding differs from
+    Bluestein's at 1e-15), index planes equal but for decision-boundary pixels."""
+    cfg = _cfg(h, w, kind, levels, mask, gain, init, qe=qe)
+    target = _target(h, w)
+    if init == "backpropagate":
+        # a real target's backpropagated start has hologram samples whose phase
+        # is set by 1e-16 rounding (chaotic for any two FFTs, see
+        # test_gpu_gs.CHAOTIC); a random-phase target is well conditioned
+        target = target * np.exp(2j * np.pi * np.random.default_rng(h).random((h, w)))
+    illum = gaussian_beam(h, w) if beam else None
+    ref_holo, ref = O.gs(cfg, target, illum)
+    with precision("fp64"):
+        holo, rep = A.run_gs(cfg, target, illum)
+    t_ref = np.array([e for _, e in ref.error_trace])
+    t_got = np.array([e for _, e in rep.error_trace])
+    assert len(t_got) == len(t_ref) == cfg.iterations + 1
+    assert np.max(np.abs(t_got - t_ref) / t_ref) < 1e-9
+    assert np.mean(holo != ref_holo) < 2e-3
+    assert abs(rep.efficiency - ref.efficiency) < 1e-9
+
+
+def test_gs_any_shape_fp32_and_1080p():
+    cfg = _cfg(108, 192, "fresnel", 8, iters=12)
+    target = _target(108, 192)
+    ref_holo, ref = O.gs(cfg, target)
+    with precision("fp32"):
+        holo, rep = A.run_gs(cfg, target)
+    t_ref = np.array([e for _, e in ref.error_trace])
+    t_got = np.array([e for _, e in rep.error_trace])
+    assert np.max(np.abs(t_got - t_ref) / t_ref) < 1e-3
+    assert np.mean(holo != ref_holo) < 1e-2
+    # a full-HD SLM plane (1080 x 1920) runs end to end and improves
+    big = _cfg(1080, 1920, "fourier", 8, iters=5)
+    with precision("fp32"):
+        holo, rep = A.run_gs(big, _target(1080, 1920))
+    tr = [e for _, e in rep.error_trace]
+    assert holo.shape == (1080, 1920) and tr[-2] < tr[0] and np.all(np.isin(holo[::97, ::89], A.states(big.slm.scheme)))
+
+
+def test_other_runners_reject_non_power_of_two_loudly():
+    cfg = _cfg(45, 60, "fourier", 2)
+    target = _target(45, 60)
+    for run, alg in ((A.run_ospr, "ospr"), (A.run_sa, "sa"), (A.run_dbs, "dbs")):
+        cfg.algorithm = alg
+        with pytest.raises(UnsupportedShapeError):
+            run(cfg, target)
