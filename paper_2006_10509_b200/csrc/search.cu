@@ -84,8 +84,8 @@ struct Draw {
 
 __device__ __forceinline__ void draw_ahead(const SearchArgs& a, Pcg64 g, Draw& d) {
     const uint32_t p = pcg_integers(g, uint64_t(a.H) * uint64_t(a.W));
-    d.m = int(p >> a.logW);
-    d.n = int(p & (a.W - 1));
+    d.m = a.pow2 ? int(p >> a.logW) : int(p / uint32_t(a.W));
+    d.n = a.pow2 ? int(p & (a.W - 1)) : int(p % uint32_t(a.W));
     d.jraw = int(pcg_integers(g, uint64_t(a.L - 1)));
     d.g = g;
     d.idx = read_index(a, (long long)d.m * a.W + d.n);   // consumed after the grid barrier
@@ -290,7 +290,8 @@ __global__ void __launch_bounds__(kSearchThreads, 1) dbs_kernel(SearchArgs a) {
             nwin = w;
             for (int k = 0; k < w; ++k) {
                 const long long p = a.order ? a.order[st.executed + k] : st.executed + k;
-                const int m = int(p >> a.logW), n = int(p & (a.W - 1));
+                const int m = a.pow2 ? int(p >> a.logW) : int(p / a.W);
+                const int n = a.pow2 ? int(p & (a.W - 1)) : int(p % a.W);
                 wp[k] = p;
                 wm[k] = m;
                 wn[k] = n;
@@ -512,7 +513,7 @@ __global__ void mask_scatter_kernel(const double* __restrict__ tgt, const double
         const long long o = offsets[blockIdx.x] + scan[i];
         R[o] = rep[p];
         t[o] = fabs(tgt[p]);
-        pos[o] = (uint32_t(p >> logW) << 16) | uint32_t(p & (W - 1));
+        pos[o] = (uint32_t(p / W) << 16) | uint32_t(p % W);   // any W (logW unused)
     }
 }
 
@@ -628,8 +629,6 @@ static int search_alloc(SearchRun& S, size_t bytes, void** out) {
 // Initial index plane + uncentred replay + masked gather (algorithms.py:217-251).
 static int search_setup(SearchRun& S, int init_mode, const cgh_pcg64& rng0, bool dbs) {
     cgh_plan* P = S.P;
-    if (!is_pow2(P->H) || !is_pow2(P->W))   // the DFT table indexing uses power-of-two masks
-        return fail(CGH_ERR_UNSUPPORTED, "SA/DBS: power-of-two planes only (got %dx%d)", P->H, P->W);
     const long long n = (long long)P->H * P->W;
     CGH_TRY(ensure(P, P->data, size_t(n) * 16));
     CGH_TRY(ensure(P, P->idx, size_t(n) * P->idx_bytes));
@@ -659,7 +658,9 @@ static int search_setup(SearchRun& S, int init_mode, const cgh_pcg64& rng0, bool
     CGH_TRY(run_col<double>(P, COL_FWD, a, 1));
 
     S.M = (long long)P->count_in;
-    S.full = (S.M == n);
+    // full masks use implicit row-major positions (shift / mask); other planes
+    // carry packed positions
+    S.full = (S.M == n) && is_pow2(P->H) && is_pow2(P->W);
     if (S.full) {
         S.R = static_cast<double2*>(P->data.p);
         S.t = static_cast<double*>(P->tgt.p);
@@ -783,6 +784,7 @@ static SearchArgs search_args(SearchRun& S) {
     a.W = P->W;
     while ((1 << a.logH) < P->H) ++a.logH;
     while ((1 << a.logW) < P->W) ++a.logW;
+    a.pow2 = (is_pow2(P->H) && is_pow2(P->W)) ? 1 : 0;
     a.M = S.M;
     a.full = S.full ? 1 : 0;
     a.R = S.R;

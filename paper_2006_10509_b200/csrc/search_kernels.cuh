@@ -34,6 +34,7 @@ struct SearchState {
 
 struct SearchArgs {
     int H, W, logH, logW;
+    int pow2;                    // both sides powers of two (index masks), else division / modulo
     long long M;                 // masked elements
     int full;                    // positions implicit (full mask, row-major)
     double2* R;                  // [M] replay at mask positions (global copy)
@@ -174,7 +175,8 @@ __device__ __forceinline__ void element_pos(const SearchArgs& a, const Slice& s,
 // twiddle product row_tw[m][mu] * col_tw[n][mv] from the 1-D tables
 __device__ __forceinline__ double2 tw_of(const double2* rt, const double2* ct, const SearchArgs& a, int m, int n, int mu,
                                          int mv) {
-    return dmul(rt[(m * mu) & (a.H - 1)], ct[(n * mv) & (a.W - 1)]);
+    if (a.pow2) return dmul(rt[(m * mu) & (a.H - 1)], ct[(n * mv) & (a.W - 1)]);
+    return dmul(rt[(m * mu) % a.H], ct[(n * mv) % a.W]);
 }
 
 __device__ __forceinline__ double dabs(double2 z) { return sqrt(z.x * z.x + z.y * z.y); }

@@ -145,10 +145,41 @@ def test_gs_any_shape_fp32_and_1080p():
     assert holo.shape == (1080, 1920) and tr[-2] < tr[0] and np.all(np.isin(holo[::97, ::89], A.states(big.slm.scheme)))
 
 
-def test_other_runners_reject_non_power_of_two_loudly():
+def test_ospr_rejects_non_power_of_two_loudly():
     cfg = _cfg(45, 60, "fourier", 2)
-    target = _target(45, 60)
-    for run, alg in ((A.run_ospr, "ospr"), (A.run_sa, "sa"), (A.run_dbs, "dbs")):
-        cfg.algorithm = alg
-        with pytest.raises(UnsupportedShapeError):
-            run(cfg, target)
+    cfg.algorithm = "ospr"
+    with pytest.raises(UnsupportedShapeError):
+        A.run_ospr(cfg, _target(45, 60))
+
+
+@pytest.mark.parametrize("h,w,kind,levels,mask", [(12, 20, "fourier", 2, False), (10, 14, "fresnel", 4, True)])
+def test_sa_any_shape_decisions_match_oracle(h, w, kind, levels, mask):
+    """SA on a non-power-of-two plane (DFT tables indexed modulo H, W; packed
+    element positions): every accept/reject decision equals the oracle's."""
+    from paper_2006_10509_b200.search import sa_call
+
+    cfg = _cfg(h, w, kind, levels, mask)
+    cfg.algorithm, cfg.proposals = "sa", 3000
+    target = _target(h, w)
+    ref_holo, ref = O.sa(cfg, target, None, log_limit=3000)
+    with precision("fp64"):
+        holo, rep = sa_call(cfg, target, None, None, None, None, log_cap=3000)
+    pix, lev, acc = rep.decisions
+    want = np.array(ref.log)
+    assert np.array_equal(pix, want[:, 0].astype(np.int64))
+    assert np.array_equal(lev, want[:, 1].astype(np.int32))
+    assert np.array_equal(acc.astype(bool), want[:, 2].astype(bool))
+    assert np.array_equal(holo, ref_holo)
+    assert abs(rep.final_error - ref.final_error) / ref.final_error < 1e-9
+
+
+@pytest.mark.parametrize("order", ["raster", "random"])
+def test_dbs_any_shape_matches_oracle(order):
+    cfg = _cfg(9, 14, "fresnel", 4, True)
+    cfg.algorithm, cfg.max_passes, cfg.scan_order = "dbs", 3, order
+    target = _target(9, 14)
+    ref_holo, ref = O.dbs(cfg, target)
+    holo, rep = A.run_dbs(cfg, target)
+    assert np.array_equal(holo, ref_holo)
+    assert abs(rep.final_error - ref.final_error) / ref.final_error < 1e-9
+    assert rep.iterations_executed == ref.iterations_executed
