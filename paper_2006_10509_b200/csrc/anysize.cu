@@ -386,6 +386,130 @@ __global__ void __launch_bounds__(AnyShape<T, M>::TF) any_row_kernel(PassArgs<T>
             }
         }
         blue_dft<T, M, E>(v, -1, N, sre, sim, t, a.tw_row);
+    } else if constexpr (MODE == ROW_OSPR_GEN) {
+        // OSPR K1 (algorithms.py:494-499): frame blockIdx.y's random-phase
+        // sub-target |T| exp(i 2 pi u), u drawn row-major over the CENTRED
+        // plane, ifftshifted into uncentred row m (centred row (m + H/2) % H,
+        // centred column c lands on uncentred column (c + N - N/2) % N; odd
+        // sides included), then the inverse row DFT.
+        const int uc = (m + a.H / 2) % a.H;
+        const int ch = (N + TF - 1) / TF, j0 = t * ch, j1 = min(N, j0 + ch);
+        if (j0 < j1) {
+            Pcg64 g = a.frame_rng[a.frame0 + blockIdx.y];
+            pcg_advance(g, uint64_t(long(uc) * N + j0));
+            int k = (j0 + N - N / 2) % N;
+            for (int j = j0; j < j1; ++j) {
+                const cx<T> z = unit_phase<T>(g);
+                const T amp = fabs(a.tgt[long(m) * N + k]);
+                sre[padx<T>(k)] = amp * z.x;
+                sim[padx<T>(k)] = amp * z.y;
+                k = k + 1 == N ? 0 : k + 1;
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < E; ++r) {
+            const int n = t + r * TF;
+            v[r] = n < N ? mk(sre[padx<T>(n)], sim[padx<T>(n)]) : mk<T>(0, 0);
+        }
+        blue_dft<T, M, E>(v, +1, N, sre, sim, t, a.tw_row);
+    } else if constexpr (MODE == ROW_OSPR_ACC) {
+        // OSPR K3 (algorithms.py:502-512): row m of every frame in
+        // [frame0, frame0 + frames): forward row DFT, |R|^2 accumulated,
+        // per-frame masked error sums of sqrt(I / i); the frame after the
+        // last adds the efficiency sums. Same per-pixel code and fixed-order
+        // reduction as row_kernel's ROW_OSPR_ACC, one CTA per row.
+        __shared__ double blk[3 * 64 + 2];
+        double* rs = red_scratch<T>(smem, Sh::FFT_BYTES);
+        const long pix0 = long(m) * N;
+        T inten[E], tv[E];
+#pragma unroll
+        for (int r = 0; r < E; ++r) {
+            const int n = t + r * TF;
+            inten[r] = (n < N && a.load_intensity) ? a.intensity[pix0 + n] : T(0);
+            tv[r] = n < N ? a.tgt[pix0 + n] : T(-0.0);
+        }
+        for (int f = 0; f < a.frames; ++f) {
+            const cx<T>* fr = a.data + long(f) * a.frame_stride + pix0;
+#pragma unroll
+            for (int r = 0; r < E; ++r) v[r] = t + r * TF < N ? fr[t + r * TF] : mk<T>(0, 0);
+            blue_dft<T, M, E>(v, -1, N, sre, sim, t, a.tw_row);
+            const T inv_n = T(1) / T(a.frame0 + f + 1);
+            T sdd = 0, spp = 0, spd = 0;
+#pragma unroll
+            for (int r = 0; r < E; ++r) {
+                if (t + r * TF >= N) continue;
+                const cx<T> R = v[r] * a.scale;
+                inten[r] += R.x * R.x + R.y * R.y;
+                if (!signbit(tv[r])) {
+                    const T p = dev_sqrt<T>(inten[r] * inv_n);
+                    const T d = p - tv[r];
+                    sdd += d * d;
+                    spp += p * p;
+                    spd += p * d;
+                }
+            }
+            double acc[3] = {double(sdd), double(spp), double(spd)};
+            block_reduce<3>(acc, rs);
+            if (t == 0) {
+                blk[3 * f + 0] = acc[0];
+                blk[3 * f + 1] = acc[1];
+                blk[3 * f + 2] = acc[2];
+            }
+        }
+        const bool tail = (a.frame0 + a.frames == a.nframes_total);
+        int nq = 3 * a.frames;
+        if (tail) {
+            const T inv_n = T(1) / T(a.nframes_total);
+            T sin_ = 0, sall = 0;
+#pragma unroll
+            for (int r = 0; r < E; ++r) {
+                if (t + r * TF >= N) continue;
+                const T p = dev_sqrt<T>(inten[r] * inv_n);
+                const T pp = p * p;
+                sall += pp;
+                if (!signbit(tv[r])) sin_ += pp;
+            }
+            double acc[2] = {double(sin_), double(sall)};
+            block_reduce<2>(acc, rs);
+            if (t == 0) {
+                blk[nq + 0] = acc[0];
+                blk[nq + 1] = acc[1];
+            }
+            nq += 2;
+        }
+        if (a.store_intensity) {
+#pragma unroll
+            for (int r = 0; r < E; ++r)
+                if (t + r * TF < N) a.intensity[pix0 + t + r * TF] = inten[r];
+        }
+        const int nblocks = gridDim.x;
+        __shared__ int last;
+        __syncthreads();
+        if (t == 0) {
+            for (int q = 0; q < nq; ++q) a.red.partials[long(q) * nblocks + blockIdx.x] = blk[q];
+            __threadfence();
+            last = (atomicAdd(a.red.counter, 1u) == unsigned(nblocks - 1));
+        }
+        __syncthreads();
+        if (last) {
+            __threadfence();
+            const double denom = *a.red.denom;
+            for (int f = 0; f < a.frames; ++f) {
+                const double sdd = sum_partials(a.red, 3 * f + 0, nblocks, rs);
+                const double spp = sum_partials(a.red, 3 * f + 1, nblocks, rs);
+                const double spd = sum_partials(a.red, 3 * f + 2, nblocks, rs);
+                if (t == 0) a.red.out[a.frame0 + f] = error_from_sums(sdd, spp, spd, denom, a.red.rescale);
+            }
+            if (tail) {
+                const double sin_ = sum_partials(a.red, 3 * a.frames + 0, nblocks, rs);
+                const double sall = sum_partials(a.red, 3 * a.frames + 1, nblocks, rs);
+                if (t == 0)
+                    a.red.out[a.nframes_total] = sall == 0.0 ? __longlong_as_double(0x7ff8000000000000LL) : sin_ / sall;
+            }
+            if (t == 0) *a.red.counter = 0u;
+        }
+        return;
     } else {   // ROW_FWD, ROW_INV, ROW_HOLO
 #pragma unroll
         for (int r = 0; r < E; ++r) v[r] = t + r * TF < N ? row[t + r * TF] : mk<T>(0, 0);
@@ -425,6 +549,15 @@ __global__ void __launch_bounds__(AnyShape<T, M>::TF) any_col_kernel(PassArgs<T>
 #pragma unroll
             for (int r = 0; r < E; ++r) v[r] = v[r] * a.scale;
         }
+    } else if constexpr (MODE == COL_HOLO) {
+        // OSPR K2: inverse column DFT -> hologram projection (+ index plane of
+        // frame blockIdx.y) -> forward column DFT
+        const long foff = long(blockIdx.y) * a.frame_stride;
+        blue_dft<T, M, E>(v, +1, N, sre, sim, t, a.tw_col);
+#pragma unroll
+        for (int r = 0; r < E; ++r)
+            if (t + r * TF < N) v[r] = holo_project<T>(a, v[r], t + r * TF, n, foff);
+        blue_dft<T, M, E>(v, -1, N, sre, sim, t, a.tw_col);
     } else {   // COL_GS, COL_FINAL (col_kernel's epilogue)
         blue_dft<T, M, E>(v, -1, N, sre, sim, t, a.tw_col);
         T sdd = 0, srr = 0, srd = 0, sall = 0;
@@ -497,7 +630,9 @@ static cudaError_t any_row_m(int mode, const PassArgs<T>& a, int frames, cudaStr
         case ROW_INV: return any_launch<T, M>(any_row_kernel<T, M, ROW_INV>, a.H, frames, st, a);
         case ROW_HOLO: return any_launch<T, M>(any_row_kernel<T, M, ROW_HOLO>, a.H, frames, st, a);
         case ROW_INIT: return any_launch<T, M>(any_row_kernel<T, M, ROW_INIT>, a.H, frames, st, a);
-        default: return cudaErrorNotSupported;   // OSPR passes: power-of-two planes only
+        case ROW_OSPR_GEN: return any_launch<T, M>(any_row_kernel<T, M, ROW_OSPR_GEN>, a.H, frames, st, a);
+        case ROW_OSPR_ACC: return any_launch<T, M>(any_row_kernel<T, M, ROW_OSPR_ACC>, a.H, 1, st, a);
+        default: return cudaErrorNotSupported;
     }
 }
 
@@ -508,6 +643,7 @@ static cudaError_t any_col_m(int mode, const PassArgs<T>& a, int frames, cudaStr
         case COL_INV: return any_launch<T, M>(any_col_kernel<T, M, COL_INV>, a.W, frames, st, a);
         case COL_GS: return any_launch<T, M>(any_col_kernel<T, M, COL_GS>, a.W, frames, st, a);
         case COL_FINAL: return any_launch<T, M>(any_col_kernel<T, M, COL_FINAL>, a.W, frames, st, a);
+        case COL_HOLO: return any_launch<T, M>(any_col_kernel<T, M, COL_HOLO>, a.W, frames, st, a);
         default: return cudaErrorNotSupported;
     }
 }

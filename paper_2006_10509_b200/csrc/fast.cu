@@ -246,7 +246,7 @@ static int encode_2d(CUtensorMap* m, void* ptr, int W, int rows, int C, int box_
 }
 
 bool fast_ospr_eligible(cgh_plan* P) {
-    if (P->prec != CGH_FP32 || P->idx_bytes != 1) return false;
+    if (P->prec != CGH_FP32 || P->idx_bytes != 1 || !is_pow2(P->H) || !is_pow2(P->W)) return false;
     const int lc = fast_lines_th(P->H, 512);
     if (lc < 1 || P->W < lc || P->H < 512 || P->W < 512 || P->W > 4096) return false;
     if (getenv("CGHB200_NO_FAST")) return false;

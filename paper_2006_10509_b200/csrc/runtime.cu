@@ -584,8 +584,6 @@ template <class T>
 static int ospr_exec(cgh_plan* P, const cgh_ospr_params* op, int64_t* tk, double* tv, int64_t cap, cgh_report* rep,
                      const cgh_callbacks* cb) {
     if (!P->target_ready) return fail(CGH_ERR_VALUE, "target not set");
-    if (!is_pow2(P->H) || !is_pow2(P->W))
-        return fail(CGH_ERR_UNSUPPORTED, "OSPR: power-of-two planes only (got %dx%d)", P->H, P->W);
     const int S = std::max(0, op->subframes);
     if (S > 0 && !op->frame_rng) return fail(CGH_ERR_VALUE, "frame streams missing");
     // reference order per frame: propagate_inverse(sub_target) -> ... -> mse_error
@@ -726,8 +724,6 @@ static int ospr_exec(cgh_plan* P, const cgh_ospr_params* op, int64_t* tk, double
 template <class T>
 static int ospr_part_exec(cgh_plan* P, const cgh_ospr_params* op, int frame0, int nframes_total, int phase,
                           int64_t* tk, double* tv, int64_t cap, cgh_report* rep) {
-    if (!is_pow2(P->H) || !is_pow2(P->W))
-        return fail(CGH_ERR_UNSUPPORTED, "OSPR: power-of-two planes only (got %dx%d)", P->H, P->W);
     if (!P->target_ready) return fail(CGH_ERR_VALUE, "target not set");
     const int m = std::max(0, op->subframes);
     if (m < 1 || m > 64) return fail(CGH_ERR_UNSUPPORTED, "a sharded OSPR part holds 1..64 subframes (got %d)", m);

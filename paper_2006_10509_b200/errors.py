@@ -44,7 +44,7 @@ class BackendUnavailableError(CghError, RuntimeError):
 
 
 class UnsupportedShapeError(CghError, NotImplementedError):
-    """Shape outside what the CUDA path implements (power-of-two sides)."""
+    """Shape outside what the CUDA path implements (plan sides 2..4096, slab planes)."""
 
 
 class DeviceError(CghError, RuntimeError):

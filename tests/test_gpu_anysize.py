@@ -145,11 +145,71 @@ def test_gs_any_shape_fp32_and_1080p():
     assert holo.shape == (1080, 1920) and tr[-2] < tr[0] and np.all(np.isin(holo[::97, ::89], A.states(big.slm.scheme)))
 
 
-def test_ospr_rejects_non_power_of_two_loudly():
-    cfg = _cfg(45, 60, "fourier", 2)
-    cfg.algorithm = "ospr"
-    with pytest.raises(UnsupportedShapeError):
-        A.run_ospr(cfg, _target(45, 60))
+@pytest.mark.parametrize("h,w,kind,levels,mask,beam,frames", [
+    (45, 60, "fourier", 2, False, False, 5),
+    (33, 31, "fresnel", 8, True, True, 4),       # odd sides: ifftshift != fftshift
+    (100, 64, "fourier", 4, True, False, 3),     # non-power-of-two rows only
+    (64, 96, "fresnel", 2, False, False, 3),     # non-power-of-two columns only
+])
+def test_ospr_any_shape_fp64_matches_oracle(h, w, kind, levels, mask, beam, frames):
+    """run_ospr (algorithms.py:473-530) on planes the radix-16 passes do not
+    take: per-frame random-phase sub-targets drawn over the centred plane and
+    ifftshifted (odd sides included), Bluestein line DFTs. Subframe index
+    planes equal the oracle's but for decision-boundary pixels; cumulative
+    per-frame errors and efficiency within 1e-9."""
+    cfg = _cfg(h, w, kind, levels, mask)
+    cfg.algorithm, cfg.subframes = "ospr", frames
+    target = _target(h, w)
+    illum = gaussian_beam(h, w) if beam else None
+    ref_frames, ref = O.ospr(cfg, target, illum)
+    with precision("fp64"):
+        got_frames, rep = A.run_ospr(cfg, target, illum)
+    assert len(got_frames) == len(ref_frames) == frames
+    for a, b in zip(got_frames, ref_frames):
+        assert a.shape == (h, w) and np.mean(a != b) < 2e-3
+    t_ref = np.array([e for _, e in ref.error_trace])
+    t_got = np.array([e for _, e in rep.error_trace])
+    assert [k for k, _ in rep.error_trace] == [k for k, _ in ref.error_trace]
+    assert np.max(np.abs(t_got - t_ref) / t_ref) < 1e-9
+    assert abs(rep.efficiency - ref.efficiency) < 1e-9
+
+
+def test_ospr_any_shape_fp32_and_1080p():
+    cfg = _cfg(108, 192, "fresnel", 2)
+    cfg.algorithm, cfg.subframes = "ospr", 6
+    target = _target(108, 192)
+    ref_frames, ref = O.ospr(cfg, target)
+    with precision("fp32"):
+        got_frames, rep = A.run_ospr(cfg, target)
+    t_ref = np.array([e for _, e in ref.error_trace])
+    t_got = np.array([e for _, e in rep.error_trace])
+    assert np.max(np.abs(t_got - t_ref) / t_ref) < 1e-3
+    assert all(np.mean(a != b) < 1e-2 for a, b in zip(got_frames, ref_frames))
+    # full-HD SLM plane, 24 subframes (more than one 64-frame group is not
+    # needed: the group loop is shape-independent)
+    big = _cfg(1080, 1920, "fourier", 2)
+    big.algorithm, big.subframes = "ospr", 24
+    with precision("fp32"):
+        frames, rep = A.run_ospr(big, _target(1080, 1920))
+    tr = [e for _, e in rep.error_trace]
+    assert len(frames) == 24 and frames[0].shape == (1080, 1920)
+    assert tr[-1] < tr[0] and 0 < rep.efficiency <= 1
+
+
+def test_ospr_any_shape_sharded_matches_single():
+    from paper_2006_10509_b200.multi import run_ospr_sharded
+    from paper_2006_10509_b200.slab import SimulatedExchange
+
+    cfg = _cfg(45, 60, "fresnel", 4, True)
+    cfg.algorithm, cfg.subframes = "ospr", 7
+    target = _target(45, 60)
+    with precision("fp64"):
+        ref_h, ref = A.run_ospr(cfg, target)
+        got_h, rep = run_ospr_sharded(cfg, target, exchange=SimulatedExchange(3))
+    assert all(np.array_equal(a, b) for a, b in zip(got_h, ref_h))
+    e1 = np.array([e for _, e in rep.error_trace])
+    e0 = np.array([e for _, e in ref.error_trace])
+    assert np.max(np.abs(e1 - e0) / e0) < 1e-12
 
 
 @pytest.mark.parametrize("h,w,kind,levels,mask", [(12, 20, "fourier", 2, False), (10, 14, "fresnel", 4, True)])
