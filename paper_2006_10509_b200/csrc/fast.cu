@@ -13,6 +13,7 @@ struct FastState {
     CUtensorMap tmap_frames;    // OSPR frames stacked: float32 [F*H][2W]
     const void* tmapf_ptr = nullptr;
     int tmapf_rows = 0;
+    int tmapf_c = 0;
     DevBuf tgt_tiled, ctr, line_state, line_part;
     const void* tgt_src = nullptr;
 };
@@ -253,19 +254,39 @@ bool fast_ospr_eligible(cgh_plan* P) {
     return encode_fn() != nullptr;
 }
 
-template <int N>
-static cudaError_t holo_launch(cgh_plan* P, const FastHoloArgs& h, const CUtensorMap& map) {
-    using S = FastShape<N, 512>;
+// OSPR K2 CTA shape for H <= 1024: 256 threads x 2 CTAs/SM (default; the two
+// CTAs' exchange barriers do not align: C2 K2 232 -> 197 us, 512^2 88 -> 58 us)
+// or, with CGHB200_HOLO_TH=512, 512 threads x 1 CTA/SM (the shape H >= 2048
+// always uses: 256 threads there would mean 2-column tiles, 16-B TMA rows).
+static int holo_th() {
+    static int th = [] {
+        const char* e = getenv("CGHB200_HOLO_TH");
+        return (e && atoi(e) == 512) ? 512 : 256;
+    }();
+    return th;
+}
+
+template <int N, int TH, int MINB>
+static cudaError_t holo_launch_th(cgh_plan* P, const FastHoloArgs& h, const CUtensorMap& map) {
+    using S = FastShape<N, TH>;
     const size_t smem = size_t(2) * ((S::LINES * S::LW + 15) / 16 * 16) * sizeof(float2);
-    auto k = fast_col_holo<N, 512, 1>;
+    auto k = fast_col_holo<N, TH, MINB>;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         attr = true;
     }
     const int tiles = h.frames * (P->W / S::LINES);
-    const int grid = std::max(1, std::min(sm_count(P->dev), tiles));
-    return launch_pdl(k, grid, 512, smem, P->st, h, map);
+    const int grid = std::max(1, std::min(MINB * sm_count(P->dev), tiles));
+    return launch_pdl(k, grid, TH, smem, P->st, h, map);
+}
+
+template <int N>
+static cudaError_t holo_launch(cgh_plan* P, const FastHoloArgs& h, const CUtensorMap& map) {
+    if constexpr (N <= 1024) {
+        if (holo_th() == 256) return holo_launch_th<N, 256, 2>(P, h, map);
+    }
+    return holo_launch_th<N, 512, 1>(P, h, map);
 }
 
 // OSPR K2 over `frames` stacked frames in the data buffer (capacity `cap` frames).
@@ -279,11 +300,12 @@ int fast_ospr_holo(cgh_plan* P, const PassArgs<float>& a, int frames, int cap, u
         CGH_TRY(ensure(P, F->ctr, 64));
         CGH_CUDA(cudaMemsetAsync(F->ctr.p, 0, 64, P->st));
     }
-    const int C = fast_lines_th(P->H, 512);
-    if (F->tmapf_ptr != P->data.p || F->tmapf_rows != cap * P->H) {
+    const int C = fast_lines_th(P->H, P->H <= 1024 ? holo_th() : 512);
+    if (F->tmapf_ptr != P->data.p || F->tmapf_rows != cap * P->H || F->tmapf_c != C) {
         CGH_TRY(encode_2d(&F->tmap_frames, P->data.p, P->W, cap * P->H, C, std::min(kFastBoxRows, P->H)));
         F->tmapf_ptr = P->data.p;
         F->tmapf_rows = cap * P->H;
+        F->tmapf_c = C;
     }
     FastHoloArgs h;
     h.data = reinterpret_cast<float2*>(a.data);

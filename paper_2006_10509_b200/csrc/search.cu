@@ -98,6 +98,8 @@ __device__ __forceinline__ double2 level_delta_s(const SearchArgs& a, const doub
     return d;
 }
 
+// P2: both sides powers of two (table indices by mask, not modulo)
+template <bool P2>
 __global__ void __launch_bounds__(kSearchThreads, 1) sa_kernel(SearchArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     SmemLayout L;
@@ -165,12 +167,12 @@ __global__ void __launch_bounds__(kSearchThreads, 1) sa_kernel(SearchArgs a) {
             element_pos(a, s, li, mu, mv);
             double2 R = s.R[li];
             if (pend) {
-                const double2 u = dmul(pd, tw_of(L.rt, L.ct, a, pm, pn, mu, mv));
+                const double2 u = dmul(pd, tw_of<P2>(L.rt, L.ct, a, pm, pn, mu, mv));
                 R.x += u.x;
                 R.y += u.y;
                 s.R[li] = R;
             }
-            const double2 u = dmul(d, tw_of(L.rt, L.ct, a, m, n, mu, mv));
+            const double2 u = dmul(d, tw_of<P2>(L.rt, L.ct, a, m, n, mu, mv));
             const double2 R1 = make_double2(R.x + u.x, R.y + u.y);
             const double t = s.t[li];
             const double d0 = dabs(R) - t, d1 = dabs(R1) - t;
@@ -240,7 +242,7 @@ __global__ void __launch_bounds__(kSearchThreads, 1) sa_kernel(SearchArgs a) {
         for (long long li = threadIdx.x; li < s.count; li += blockDim.x) {
             int mu, mv;
             element_pos(a, s, li, mu, mv);
-            const double2 u = dmul(pd, tw_of(L.rt, L.ct, a, st.pend_m, st.pend_n, mu, mv));
+            const double2 u = dmul(pd, tw_of<P2>(L.rt, L.ct, a, st.pend_m, st.pend_n, mu, mv));
             s.R[li].x += u.x;
             s.R[li].y += u.y;
         }
@@ -257,6 +259,7 @@ __global__ void __launch_bounds__(kSearchThreads, 1) sa_kernel(SearchArgs a) {
 // ---------------------------------------------------------------- DBS
 // Window of up to kMaxWindow pixels evaluated against the current state; the
 // first improving pixel is committed, later pixels are re-evaluated.
+template <bool P2>
 __global__ void __launch_bounds__(kSearchThreads, 1) dbs_kernel(SearchArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     SmemLayout L;
@@ -313,7 +316,7 @@ __global__ void __launch_bounds__(kSearchThreads, 1) dbs_kernel(SearchArgs a) {
             for (long long li = threadIdx.x; li < s.count; li += blockDim.x) {
                 int mu, mv;
                 element_pos(a, s, li, mu, mv);
-                const double2 u = dmul(pdel, tw_of(L.rt, L.ct, a, pm, pn, mu, mv));
+                const double2 u = dmul(pdel, tw_of<P2>(L.rt, L.ct, a, pm, pn, mu, mv));
                 s.R[li].x += u.x;
                 s.R[li].y += u.y;
             }
@@ -343,7 +346,7 @@ __global__ void __launch_bounds__(kSearchThreads, 1) dbs_kernel(SearchArgs a) {
                         if (k < W) {
                             const int jv = wvalid[k * 2] ? 0 : 1;
                             if (wvalid[k * 2 + jv]) {
-                                const double2 w = tw_of(L.rt, L.ct, a, wm[k], wn[k], mu, mv);
+                                const double2 w = tw_of<P2>(L.rt, L.ct, a, wm[k], wn[k], mu, mv);
                                 const double2 u = dmul(wd[k * 2 + jv], w);
                                 const double d1 = dabs(make_double2(R.x + u.x, R.y + u.y)) - t;
                                 acc[kk] += d1 * d1 - b0;
@@ -377,7 +380,7 @@ __global__ void __launch_bounds__(kSearchThreads, 1) dbs_kernel(SearchArgs a) {
                 element_pos(a, s, li, mu, mv);
                 const double2 R = s.R[li];
                 const double t = s.t[li];
-                const double2 w = tw_of(L.rt, L.ct, a, m, n, mu, mv);
+                const double2 w = tw_of<P2>(L.rt, L.ct, a, m, n, mu, mv);
                 const double d0 = dabs(R) - t;
                 const double b0 = d0 * d0;
 #pragma unroll
@@ -456,7 +459,7 @@ __global__ void __launch_bounds__(kSearchThreads, 1) dbs_kernel(SearchArgs a) {
         for (long long li = threadIdx.x; li < s.count; li += blockDim.x) {
             int mu, mv;
             element_pos(a, s, li, mu, mv);
-            const double2 u = dmul(pd, tw_of(L.rt, L.ct, a, st.pend_m, st.pend_n, mu, mv));
+            const double2 u = dmul(pd, tw_of<P2>(L.rt, L.ct, a, st.pend_m, st.pend_n, mu, mv));
             s.R[li].x += u.x;
             s.R[li].y += u.y;
         }
@@ -807,7 +810,8 @@ static SearchArgs search_args(SearchRun& S) {
 
 static int launch_search(SearchRun& S, bool dbs, SearchArgs& a) {
     cgh_plan* P = S.P;
-    void* fn = dbs ? (void*)dbs_kernel : (void*)sa_kernel;
+    void* fn = a.pow2 ? (dbs ? (void*)dbs_kernel<true> : (void*)sa_kernel<true>)
+                      : (dbs ? (void*)dbs_kernel<false> : (void*)sa_kernel<false>);
     CGH_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(S.smem)));
     void* args[] = {&a};
     if (P->profiling) CGH_TRY(prof_mark(P, dbs ? 17 : 16, true));

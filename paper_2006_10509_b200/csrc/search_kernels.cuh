@@ -173,10 +173,11 @@ __device__ __forceinline__ void element_pos(const SearchArgs& a, const Slice& s,
 }
 
 // twiddle product row_tw[m][mu] * col_tw[n][mv] from the 1-D tables
+template <bool P2>
 __device__ __forceinline__ double2 tw_of(const double2* rt, const double2* ct, const SearchArgs& a, int m, int n, int mu,
                                          int mv) {
-    if (a.pow2) return dmul(rt[(m * mu) & (a.H - 1)], ct[(n * mv) & (a.W - 1)]);
-    return dmul(rt[(m * mu) % a.H], ct[(n * mv) % a.W]);
+    if constexpr (P2) return dmul(rt[(m * mu) & (a.H - 1)], ct[(n * mv) & (a.W - 1)]);
+    else return dmul(rt[(m * mu) % a.H], ct[(n * mv) % a.W]);
 }
 
 __device__ __forceinline__ double dabs(double2 z) { return sqrt(z.x * z.x + z.y * z.y); }
