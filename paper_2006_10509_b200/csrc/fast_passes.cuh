@@ -677,7 +677,12 @@ __global__ void __launch_bounds__(TH, MINB) fast_col_holo(FastHoloArgs a, const 
     extern __shared__ __align__(128) float2 fsm[];
     __shared__ __align__(8) uint64_t full[2];
     __shared__ int tileq[2];
+    __shared__ float2 sst[256];   // state table (uint8 index planes: <= 256 states)
     const int tid = threadIdx.x, t = tid / C, c = tid - t * C;
+    for (int k = tid; k < a.scheme.n && k < 256; k += TH) {
+        const cx<float> z = state_value<float>(a.scheme, k);
+        sst[k] = make_float2(z.x, z.y);
+    }
     const int pt = padc(t);
     const int cgroups = a.W / C;
     const int ntiles = a.frames * cgroups;
@@ -749,7 +754,8 @@ __global__ void __launch_bounds__(TH, MINB) fast_col_holo(FastHoloArgs a, const 
             if (a.binary) k = h.x < 0.0f ? 1 : 0;   // PhaseOnly(2, 0): |arg| > pi/2 <=> Re < 0 (up to rounding at Re = 0)
             else k = quantize_index<float>(a.scheme, h);
             ip[size_t(m) * a.W] = uint8_t(k);
-            cx<float> sv = state_value<float>(a.scheme, k);
+            const float2 z = sst[k];   // shared copy: no dependent global load per pixel
+            cx<float> sv = mk(z.x, z.y);
             if (fres) sv = cmul(sv, q);
             v[r] = sv;
         }
