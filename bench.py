@@ -9,9 +9,13 @@ resident in HBM. value = GS iterations/s summed over all ranks.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-N > 1 runs under torchrun, one process per GPU; each rank generates its own
-hologram (seed 1 + rank): replicas, weak scaling, no data-path collective
-(the path does not shard below one hologram at this size).
+N > 1 runs one process per GPU: under the driver's torchrun (WORLD_SIZE must
+equal N), or, launched plainly, bench.py re-executes itself through
+torch.distributed.run with N ranks (127.0.0.1 rendezvous); fewer than N
+visible GPUs is an error. Each rank generates its own C3 hologram (seed
+1 + rank): replicas, weak scaling, no data-path collective (the path does not
+shard below one hologram at this size). The C5, C6 and
+sharded-OSPR legs cover the workloads that do shard.
 
 Extra objects on the JSON line: e2e (same metric through the drop-in
 ``run_gs`` with host numpy buffers), roofline (dominant pass, live CUDA-event
@@ -56,6 +60,61 @@ def peaks():
         return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:  # noqa: BLE001
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def free_port():
+    import socket
+
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def launcher_argv(argv, n, port):
+    """torch.distributed.run command that re-executes this script on n ranks."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+            "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + list(argv)
+
+
+def ensure_world(args, argv):
+    """--gpus N: check an existing torchrun world, or spawn one. Returns an
+    exit code when this process only launched the ranks, else None."""
+    if "WORLD_SIZE" in os.environ:
+        world = int(os.environ["WORLD_SIZE"])
+        if world != args.gpus:
+            print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+            return 2
+        return None
+    if args.gpus <= 1 or args.impl == "reference":   # the reference arm runs on rank 0 alone
+        return None
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < args.gpus and not args.launch_check:
+        print(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible GPUs, found {have}", file=sys.stderr)
+        return 2
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")            # communicator lines: one per rank
+    return subprocess.call(launcher_argv(argv, args.gpus, free_port()), env=env)
+
+
+def launch_check():
+    """--launch-check (tests, CPU): every rank joins a gloo group and rank 0
+    prints the world it saw; no GPU work."""
+    import torch
+    import torch.distributed as dist
+
+    world, rank, _ = dist_env()
+    if world > 1:
+        dist.init_process_group("gloo")
+        t = torch.tensor([float(rank)])
+        dist.all_reduce(t)
+        ranks = float(t.item())
+        dist.destroy_process_group()
+    else:
+        ranks = 0.0
+    if rank == 0:
+        print(json.dumps({"launch_check": True, "n_gpus": world, "rank_sum": ranks}), flush=True)
 
 
 def dist_env():
@@ -202,6 +261,8 @@ def run_ours(args):
     if world > 1 or FORCE_DIST:
         import torch.distributed as dist
 
+        os.environ.setdefault("NCCL_DEBUG", "INFO")    # communicator lines: the driver's per-rank check
+
         import datetime
 
         # finite watchdog timeout: a rank that fails inside a collective leg
@@ -294,6 +355,32 @@ def run_ours(args):
                                       "achieved": GS_BYTES_PER_PX * hw / (iter_ms / 1000.0) / 1e9,
                                       "frac": GS_BYTES_PER_PX * hw / (iter_ms / 1000.0) / 1e9 / peak},
                     "passes_ms": {k: v[0] / max(1, v[1]) for k, v in passes.items()}}
+
+    # the fp64 parity mode (complex128 passes; index planes bit-exact against
+    # the reference at C3): same workload, 72 B/px algorithmic per iteration
+    gs64 = None
+    if not args.no_fp64:
+        plan64 = GenerationPlan(cfg, (N_PX, N_PX), precision=_native.FP64, device=local)
+        plan64.set_target(target)
+        plan64.gs(seed=seed)                 # warm
+        ms64, l64 = [], 0
+        barrier()
+        for _ in range(max(2, min(5, args.steps // 8))):
+            flush.zero_()
+            torch.cuda.synchronize()
+            r64, _ = plan64.gs(seed=seed)
+            ms64.append(r64.device_ms)
+            l64 += r64.kernel_launches
+        t64 = max_over_ranks(sum(ms64))
+        it64 = sum(ms64) / len(ms64) / ITERS
+        b64 = 2 * GS_BYTES_PER_PX * hw
+        gs64 = {"metric": "GS iterations/s, fp64 parity mode (C3 workload in complex128)",
+                "value": world * len(ms64) * ITERS / (t64 / 1000.0), "unit": "iter/s", "dtype": "f64",
+                "steps": len(ms64), "ms_per_step": sum(ms64) / len(ms64), "gpu_launches_per_step": l64 / len(ms64),
+                "roofline": {"bound": "hbm", "achieved": b64 / (it64 / 1000.0) / 1e9, "peak": peak, "unit": "GB/s",
+                             "frac": b64 / (it64 / 1000.0) / 1e9 / peak, "algorithmic_bytes_per_iteration": b64,
+                             "ms_per_iteration": it64}}
+        plan64.close()
 
     # e2e: the drop-in run_gs with host numpy buffers (H2D target+mask, D2H indices)
     e2e = None
@@ -562,7 +649,7 @@ def run_ours(args):
                            "l2": "256 MB device write between timed steps (excluded from step time)"},
                 "gpu_launches": launches, "wall_s_timed": t_wall,
                 "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clk.summary(), "ospr": ospr,
-                "search": search, "c5": c5, "c6": c6, "hgi": hgi,
+                "search": search, "c5": c5, "c6": c6, "hgi": hgi, "gs_fp64": gs64,
                 "ospr_sharded": ospr_sh}
         print(json.dumps(line), flush=True)
     plan.close()
@@ -583,11 +670,19 @@ def main():
     ap.add_argument("--no-c5", action="store_true")
     ap.add_argument("--no-c6", action="store_true")
     ap.add_argument("--no-hgi", action="store_true")
+    ap.add_argument("--no-fp64", action="store_true")
+    ap.add_argument("--launch-check", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--c5-sample", type=int, default=8, help="targets timed per rank (of its block of 64/N)")
     ap.add_argument("--c6-steps", type=int, default=3)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    rc = ensure_world(args, sys.argv[1:])
+    if rc is not None:
+        sys.exit(rc)
+    if args.launch_check:
+        launch_check()
+        return
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -243,7 +243,7 @@ int cgh_best_delta(int32_t device, const double *replay_m, const double *target_
  * (global). Pass modes: 0 random-phase init [-> snap] -> forward; 1 hologram
  * pass (inverse -> beam*x/|x| [-> snap] -> forward); 2 replay pass (forward ->
  * error sums + amplitude projection -> inverse); 3 final replay (sums only);
- * 4 inverse (backpropagation start). Sums: 4 doubles {S_dd, S_rr, S_rd,
+ * 4 inverse (backpropagation start); 6 forward, unscaled (transform only). Sums: 4 doubles {S_dd, S_rr, S_rd,
  * S_all} of this rank written to the device pointer `sums` (modes 2, 3). */
 typedef struct cgh_slab cgh_slab;
 int cgh_slab_create(const cgh_problem *pb, int32_t world, int32_t rank, void *stream, cgh_slab **out);

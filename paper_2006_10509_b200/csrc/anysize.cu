@@ -358,8 +358,9 @@ __global__ void __launch_bounds__(AnyShape<T, M>::TF) any_row_kernel(PassArgs<T>
             for (int j = j0; j < j1; ++j) {
                 const cx<T> z = unit_phase<T>(g);
                 const T amp = a.beam ? a.beam[long(m) * N + j] : T(1);
-                sre[padx<T>(j)] = amp * z.x;
-                sim[padx<T>(j)] = amp * z.y;
+                const cx<T> h = beam_zero_signs(amp, mk(amp * z.x, amp * z.y));
+                sre[padx<T>(j)] = h.x;
+                sim[padx<T>(j)] = h.y;
             }
         }
         __syncthreads();

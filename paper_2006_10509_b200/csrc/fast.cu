@@ -2,6 +2,7 @@
 #include <cudaTypedefs.h>
 
 #include "fast_passes.cuh"
+#include "launch.cuh"
 #include "runtime.cuh"
 
 namespace cgh {
@@ -166,11 +167,7 @@ static cudaError_t row_launch_s(cgh_plan* P, const FastArgs& f) {
     using S = FastShape<N, kRowTH>;
     const size_t smem = (size_t(TwTables<N, kRowTH>::WORDS) + size_t(S::LINES) * ((S::LW + 15) / 16 * 16)) * sizeof(float2);
     auto k = fast_row_holo_s<N, kRowTH, MINB>;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        attr = true;
-    }
+    if (cudaError_t e = ensure_smem_attr<fast_row_holo_s<N, kRowTH, MINB>>(smem); e != cudaSuccess) return e;
     const int grid = std::max(1, std::min(MINB * sm_count(P->dev), P->H / S::LINES));
     return launch_pdl(k, grid, kRowTH, smem, P->st, f);
 }
@@ -191,11 +188,7 @@ static cudaError_t row_launch(cgh_plan* P, const FastArgs& f) {
     using S = FastShape<N, kRowTH>;
     const size_t smem = size_t(3) * S::LINES * ((S::LW + 15) / 16 * 16) * sizeof(float2);
     auto k = fast_row_holo<N, kRowTH, kRowMinB>;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        attr = true;
-    }
+    if (cudaError_t e = ensure_smem_attr<fast_row_holo<N, kRowTH, kRowMinB>>(smem); e != cudaSuccess) return e;
     const int tiles = P->H / S::LINES;   // row groups per CTA = S::LINES
     const int grid = std::max(1, std::min(kRowMinB * sm_count(P->dev), tiles));
     return launch_pdl(k, grid, kRowTH, smem, P->st, f);
@@ -207,11 +200,7 @@ static cudaError_t col_launch_m(cgh_plan* P, const FastArgs& f) {
     FastState* F = static_cast<FastState*>(P->fast);
     const size_t smem = size_t(2) * FastSlots<N, TH>::COL * sizeof(float2);
     auto k = fast_col_gs<N, TH, MINB, MODE>;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        attr = true;
-    }
+    if (cudaError_t e = ensure_smem_attr<fast_col_gs<N, TH, MINB, MODE>>(smem); e != cudaSuccess) return e;
     const int tiles = P->W / S::LINES;
     const int grid = std::max(1, std::min(MINB * sm_count(P->dev), tiles));
     return launch_pdl(k, grid, TH, smem, P->st, f, F->tmap);
@@ -271,11 +260,7 @@ static cudaError_t holo_launch_th(cgh_plan* P, const FastHoloArgs& h, const CUte
     using S = FastShape<N, TH>;
     const size_t smem = size_t(2) * ((S::LINES * S::LW + 15) / 16 * 16) * sizeof(float2);
     auto k = fast_col_holo<N, TH, MINB>;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        attr = true;
-    }
+    if (cudaError_t e = ensure_smem_attr<fast_col_holo<N, TH, MINB>>(smem); e != cudaSuccess) return e;
     const int tiles = h.frames * (P->W / S::LINES);
     const int grid = std::max(1, std::min(MINB * sm_count(P->dev), tiles));
     return launch_pdl(k, grid, TH, smem, P->st, h, map);
@@ -343,11 +328,7 @@ static cudaError_t gen_launch(cgh_plan* P, const FastOsprArgs& o) {
     using S = FastShape<N, kOsprTH>;
     const size_t smem = size_t(S::LINES) * ((S::LW + 15) / 16 * 16) * sizeof(float2);
     auto k = fast_ospr_gen<N, kOsprTH, kOsprMinB>;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        attr = true;
-    }
+    if (cudaError_t e = ensure_smem_attr<fast_ospr_gen<N, kOsprTH, kOsprMinB>>(smem); e != cudaSuccess) return e;
     const int grid = std::max(1, std::min(kOsprMinB * sm_count(P->dev), (o.frames * o.H + S::LINES - 1) / S::LINES));
     return launch_pdl(k, grid, kOsprTH, smem, P->st, o);
 }
@@ -357,11 +338,7 @@ static cudaError_t acc_launch(cgh_plan* P, const FastOsprArgs& o) {
     using S = FastShape<N, kOsprTH>;
     const size_t smem = (size_t(TwTables<N, kOsprTH>::WORDS) + size_t(S::LINES) * 2 * ((S::LW + 15) / 16 * 16)) * sizeof(float2);
     auto k = fast_ospr_acc<N, kOsprTH, kOsprMinB>;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        attr = true;
-    }
+    if (cudaError_t e = ensure_smem_attr<fast_ospr_acc<N, kOsprTH, kOsprMinB>>(smem); e != cudaSuccess) return e;
     const int grid = std::max(1, std::min(kOsprMinB * sm_count(P->dev), (o.H + S::LINES - 1) / S::LINES));
     return launch_pdl(k, grid, kOsprTH, smem, P->st, o);
 }

@@ -750,8 +750,11 @@ __global__ void __launch_bounds__(TH, MINB) fast_col_holo(FastHoloArgs a, const 
             } else {
                 h = mk(amp, 0.0f);
             }
+            h = beam_zero_signs(amp, h);
             int k;
-            if (a.binary) k = h.x < 0.0f ? 1 : 0;   // PhaseOnly(2, 0): |arg| > pi/2 <=> Re < 0 (up to rounding at Re = 0)
+            // PhaseOnly(2, 0): |arg| > pi/2 <=> Re < 0; Re == 0 (a zero beam's
+            // signed zeros, or arg = +-pi/2 ties) takes the reference formula
+            if (a.binary && h.x != 0.0f) k = h.x < 0.0f ? 1 : 0;
             else k = quantize_index<float>(a.scheme, h);
             ip[size_t(m) * a.W] = uint8_t(k);
             const float2 z = sst[k];   // shared copy: no dependent global load per pixel

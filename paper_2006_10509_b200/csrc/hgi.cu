@@ -80,11 +80,18 @@ __device__ __forceinline__ uint32_t tab_apply(const uint32_t* t, uint32_t c) {
     return t[c & 255u] ^ t[256 + (c >> 8 & 255u)] ^ t[512 + (c >> 16 & 255u)] ^ t[768 + (c >> 24)];
 }
 
-// payload[p] = states[idx[p]] (complex128 as two doubles)
+// payload[p] = states[idx[p]] (complex128 as two doubles). An index outside
+// the table (the reference's states[indices] raises IndexError) sets *bad and
+// is not read.
 __global__ void hgi_expand_kernel(const void* __restrict__ idx, int idx_bytes, long long n,
-                                  const double2* __restrict__ states, double2* __restrict__ out) {
+                                  const double2* __restrict__ states, int n_states, double2* __restrict__ out,
+                                  unsigned* __restrict__ bad) {
     for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x) {
         const int k = idx_bytes == 1 ? int(static_cast<const uint8_t*>(idx)[p]) : static_cast<const int32_t*>(idx)[p];
+        if (k < 0 || k >= n_states) {
+            *bad = 1u;
+            continue;
+        }
         out[p] = states[k];
     }
 }
@@ -94,9 +101,10 @@ __global__ void hgi_expand_kernel(const void* __restrict__ idx, int idx_bytes, l
 // (a zero record for q < pad). k_rec: raw CRC of each state's 16 bytes.
 __global__ void __launch_bounds__(kCrcBlock) hgi_crc_kernel(const void* __restrict__ idx, int idx_bytes, long long n,
                                                             long long pad, const uint32_t* __restrict__ k_rec,
-                                                            const uint32_t* __restrict__ s16_g,
+                                                            int n_states, const uint32_t* __restrict__ s16_g,
                                                             const uint32_t* __restrict__ sch_g,
-                                                            uint32_t* __restrict__ block_crc) {
+                                                            uint32_t* __restrict__ block_crc,
+                                                            unsigned* __restrict__ bad) {
     __shared__ uint32_t s16[1024], sch[1024], part[kCrcBlock];
     for (int i = threadIdx.x; i < 1024; i += blockDim.x) {
         s16[i] = s16_g[i];
@@ -110,7 +118,8 @@ __global__ void __launch_bounds__(kCrcBlock) hgi_crc_kernel(const void* __restri
         uint32_t kr = 0;
         if (p >= 0 && p < n) {
             const int k = idx_bytes == 1 ? int(static_cast<const uint8_t*>(idx)[p]) : static_cast<const int32_t*>(idx)[p];
-            kr = k_rec[k];
+            if (k >= 0 && k < n_states) kr = k_rec[k];
+            else *bad = 1u;
         }
         c = tab_apply(s16, c) ^ kr;
     }
@@ -180,27 +189,30 @@ int cgh_hgi_payload(int32_t device, const void* idx, int32_t idx_bytes, int64_t 
     HGI_CUDA(cudaMallocAsync(&d_states, size_t(n_states) * 16, st));
     HGI_CUDA(cudaMallocAsync(&d_k, size_t(n_states) * 4, st));
     HGI_CUDA(cudaMallocAsync(&d_tabs, tabs.size() * 4, st));
-    HGI_CUDA(cudaMallocAsync(&d_blk, size_t(nblocks) * 4, st));
+    HGI_CUDA(cudaMallocAsync(&d_blk, size_t(nblocks) * 4 + 16, st));
+    unsigned* d_bad = reinterpret_cast<unsigned*>(static_cast<char*>(d_blk) + size_t(nblocks) * 4);
+    HGI_CUDA(cudaMemsetAsync(d_bad, 0, 4, st));
     HGI_CUDA(cudaMemcpyAsync(d_idx, idx, ib, cudaMemcpyHostToDevice, st));
     HGI_CUDA(cudaMemcpyAsync(d_states, states, size_t(n_states) * 16, cudaMemcpyHostToDevice, st));
     HGI_CUDA(cudaMemcpyAsync(d_k, k.data(), size_t(n_states) * 4, cudaMemcpyHostToDevice, st));
     HGI_CUDA(cudaMemcpyAsync(d_tabs, tabs.data(), tabs.size() * 4, cudaMemcpyHostToDevice, st));
     hgi_crc_kernel<<<unsigned(nblocks), kCrcBlock, 0, st>>>(d_idx, idx_bytes, count, pad, static_cast<uint32_t*>(d_k),
-                                                            static_cast<uint32_t*>(d_tabs),
+                                                            n_states, static_cast<uint32_t*>(d_tabs),
                                                             static_cast<uint32_t*>(d_tabs) + 1024,
-                                                            static_cast<uint32_t*>(d_blk));
+                                                            static_cast<uint32_t*>(d_blk), d_bad);
     HGI_CUDA(cudaGetLastError());
     if (out_payload && count > 0) {
         HGI_CUDA(cudaMallocAsync(&d_pay, size_t(count) * 16, st));
         hgi_expand_kernel<<<grid_for(count), 256, 0, st>>>(d_idx, idx_bytes, count, static_cast<double2*>(d_states),
-                                                          static_cast<double2*>(d_pay));
+                                                          n_states, static_cast<double2*>(d_pay), d_bad);
         HGI_CUDA(cudaGetLastError());
         HGI_CUDA(cudaMemcpyAsync(out_payload, d_pay, size_t(count) * 16, cudaMemcpyDeviceToHost, st));
     }
-    std::vector<uint32_t> blk(static_cast<size_t>(nblocks) + 0);
-    HGI_CUDA(cudaMemcpyAsync(blk.data(), d_blk, size_t(nblocks) * 4, cudaMemcpyDeviceToHost, st));
+    std::vector<uint32_t> blk(static_cast<size_t>(nblocks) + 1);
+    HGI_CUDA(cudaMemcpyAsync(blk.data(), d_blk, size_t(nblocks) * 4 + 4, cudaMemcpyDeviceToHost, st));
     HGI_CUDA(cudaStreamSynchronize(st));
     cleanup();
+    if (blk[size_t(nblocks)] != 0u) return fail(CGH_ERR_VALUE, "index outside the state table (%d states)", n_states);
 #undef HGI_CUDA
     // fold the block registers (each covers per_block records) and condition
     std::vector<uint32_t> sb(1024);

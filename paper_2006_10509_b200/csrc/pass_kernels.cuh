@@ -30,8 +30,10 @@ __device__ __forceinline__ cx<T> unit_phase(Pcg64& g) {
 }
 
 // ============================================================== row kernel
+// Launch bound = the CTA size launch_row_n uses (max(TF, 256) threads: one
+// 4096-point complex128 line takes 512 threads at 8 elements each).
 template <class T, int N, int MODE>
-__global__ void __launch_bounds__(256) row_kernel(PassArgs<T> a) {
+__global__ void __launch_bounds__(LineShape<T, N>::TF >= 256 ? LineShape<T, N>::TF : 256) row_kernel(PassArgs<T> a) {
     using Sh = LineShape<T, N>;
     constexpr int E = Sh::E, TF = Sh::TF;
     constexpr int WORDS = line_words<T, N>();
@@ -97,8 +99,10 @@ __global__ void __launch_bounds__(256) row_kernel(PassArgs<T> a) {
                     amp = fabs(a.tgt[long(m) * N + pos]);
                 }
                 const int p = padx<T>(pos);
-                sre[p] = amp * z.x;
-                sim[p] = amp * z.y;
+                cx<T> h = mk(amp * z.x, amp * z.y);
+                if constexpr (MODE == ROW_INIT) h = beam_zero_signs(amp, h);
+                sre[p] = h.x;
+                sim[p] = h.y;
             }
         }
         __syncthreads();
@@ -343,7 +347,10 @@ cudaError_t launch_row_n(const PassArgs<T>& a, int frames, cudaStream_t st) {
     const int lines = LaunchShape<T, N>::row_lines(a.H);
     const size_t sm = row_smem<T, N>(lines);
     auto k = row_kernel<T, N, MODE>;
-    if (sm > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+    if (sm > 48 * 1024) {
+        const cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+        if (e != cudaSuccess) return e;
+    }
     dim3 grid((a.H + lines - 1) / lines, MODE == ROW_OSPR_ACC ? 1 : frames);
     k<<<grid, lines * LineShape<T, N>::TF, sm, st>>>(a);
     return cudaGetLastError();
@@ -354,7 +361,10 @@ cudaError_t launch_col_n(const PassArgs<T>& a, int frames, cudaStream_t st) {
     const int C = LaunchShape<T, N>::col_cols(a.W);
     const size_t sm = row_smem<T, N>(C);
     auto k = col_kernel<T, N, MODE>;
-    if (sm > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+    if (sm > 48 * 1024) {
+        const cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+        if (e != cudaSuccess) return e;
+    }
     dim3 grid((a.W + C - 1) / C, frames);
     k<<<grid, C * LineShape<T, N>::TF, sm, st>>>(a);
     return cudaGetLastError();

@@ -139,6 +139,16 @@ __device__ __forceinline__ int quantize_index(const SchemeDev& s, cx<T> z) {
     return best;
 }
 
+// numpy's (beam + 0j) * e for a phasor e = (c, s) (algorithms.py:135,184,501:
+// a real beam array times a complex array): (b c - 0 s, b s + 0 c). Given
+// h = (b c, b s) this differs only where b == 0: the zero components then take
+// their signs from IEEE zero addition, e.g. e in the second quadrant gives
+// -0 + 0i, whose angle is pi (quantize_indices snaps it to the level at pi).
+template <class T>
+__device__ __forceinline__ cx<T> beam_zero_signs(T amp, cx<T> h) {
+    return amp == T(0) ? mk(h.x - h.y, h.y + h.x) : h;
+}
+
 // Hologram-plane projection at pixel (m, n) of x = inverse-transform value
 // (unscaled): h = beam * exp(i angle(x conj q)) [-> snap] -> h q.
 // Mirrors algorithms.py:181-184 / 500-501 (propagate_inverse, angle, quantize).
@@ -163,6 +173,7 @@ __device__ __forceinline__ cx<T> holo_project(const PassArgs<T>& a, cx<T> x, int
     } else {
         h = mk(amp, T(0));
     }
+    if (SNAP) h = beam_zero_signs(amp, h);
     if (SNAP && a.field_out) a.field_out[(long)m * a.W + n] = h;
     if (SNAP && a.quantize) {
         const int k = quantize_index<T>(a.scheme, h);

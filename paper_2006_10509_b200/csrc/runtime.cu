@@ -726,7 +726,7 @@ static int ospr_part_exec(cgh_plan* P, const cgh_ospr_params* op, int frame0, in
                           int64_t* tk, double* tv, int64_t cap, cgh_report* rep) {
     if (!P->target_ready) return fail(CGH_ERR_VALUE, "target not set");
     const int m = std::max(0, op->subframes);
-    if (m < 1 || m > 64) return fail(CGH_ERR_UNSUPPORTED, "a sharded OSPR part holds 1..64 subframes (got %d)", m);
+    if (m < 1) return fail(CGH_ERR_VALUE, "a sharded OSPR part holds at least one subframe (got %d)", m);
     if (frame0 < 0 || frame0 + m > nframes_total) return fail(CGH_ERR_VALUE, "frames [%d, %d) outside %d", frame0, frame0 + m, nframes_total);
     if (phase != 1 && phase != 2) return fail(CGH_ERR_VALUE, "phase must be 1 or 2");
     if (P->nf_all > 0) return fail(CGH_ERR_NONFINITE, "target contains NaN or Inf");
@@ -782,19 +782,25 @@ static int ospr_part_exec(cgh_plan* P, const cgh_ospr_params* op, int frame0, in
         if (!fast_done) CGH_TRY(run_col<T>(P, COL_HOLO, b, m));
         P->idx_frames = m;
     }
-    // K3: phase 1 from a zero base, phase 2 from the base the caller loaded
-    PassArgs<T> c = a;
-    c.frame0 = phase == 1 ? 0 : frame0;
-    c.nframes_total = phase == 1 ? m : nframes_total;
-    c.load_intensity = phase == 2 ? 1 : 0;
-    c.store_intensity = 1;
+    // K3: phase 1 from a zero base, phase 2 from the base the caller loaded;
+    // groups of <= 64 resident subframes (the per-frame partial slots), the
+    // intensity carried between groups as in ospr_exec
     bool fast = false;
     if constexpr (sizeof(T) == 4) fast = fast_ospr_eligible(P);
-    if constexpr (sizeof(T) == 4) {
-        if (fast) CGH_TRY(fast_ospr_acc(P, c));
-        else CGH_TRY(run_row<T>(P, ROW_OSPR_ACC, c, 1));
-    } else {
-        CGH_TRY(run_row<T>(P, ROW_OSPR_ACC, c, 1));
+    for (int g0 = 0; g0 < m; g0 += 64) {
+        PassArgs<T> c = a;
+        c.data = a.data + size_t(g0) * n;
+        c.frames = std::min(64, m - g0);
+        c.frame0 = (phase == 1 ? 0 : frame0) + g0;
+        c.nframes_total = phase == 1 ? m : nframes_total;
+        c.load_intensity = (phase == 2 || g0 > 0) ? 1 : 0;
+        c.store_intensity = 1;
+        if constexpr (sizeof(T) == 4) {
+            if (fast) CGH_TRY(fast_ospr_acc(P, c));
+            else CGH_TRY(run_row<T>(P, ROW_OSPR_ACC, c, 1));
+        } else {
+            CGH_TRY(run_row<T>(P, ROW_OSPR_ACC, c, 1));
+        }
     }
     CGH_CUDA(cudaEventRecord(P->ev1, P->st));
     CGH_CUDA(cudaEventSynchronize(P->ev1));

@@ -190,7 +190,7 @@ int slab_set_local(cgh_slab* S, const double* tgt, const double* beam) {
 
 template <class T>
 int slab_pass(cgh_slab* S, int mode, void* data, const cgh_gs_params* gp, int quantize, void* idx_out, double* sums) {
-    if (mode < SLAB_INIT || mode > SLAB_INV) return fail(CGH_ERR_VALUE, "bad slab pass mode %d", mode);
+    if (mode < SLAB_INIT || mode > SLAB_FWD || mode == SLAB_HOLO_SNAP) return fail(CGH_ERR_VALUE, "bad slab pass mode %d", mode);
     if ((mode == SLAB_GS || mode == SLAB_FINAL) && (!S->ready || !sums))
         return fail(CGH_ERR_VALUE, "replay passes need the local target (cgh_slab_set_local) and a sums pointer");
     if (!data) return fail(CGH_ERR_VALUE, "null slab buffer");

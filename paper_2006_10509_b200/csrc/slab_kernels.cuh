@@ -18,6 +18,7 @@
 #include <algorithm>
 #include <type_traits>
 
+#include "launch.cuh"
 #include "pass_kernels.cuh"
 
 namespace cgh {
@@ -29,6 +30,7 @@ enum SlabMode {
     SLAB_FINAL = 3,   // forward -> error + efficiency sums (no store)
     SLAB_INV = 4,     // inverse, scaled (backpropagation start)
     SLAB_HOLO_SNAP = 5,   // internal: SLAB_HOLO with snapping (chosen by slab_launch_n when quantize is set)
+    SLAB_FWD = 6,     // forward, unscaled (transform-only: line FFT checks against numpy.fft.fft)
 };
 
 template <class T, int N>
@@ -124,8 +126,9 @@ __global__ void __launch_bounds__(SlabShape<T, N>::THREADS) slab_kernel(SlabArgs
                     const int pos = t * E + e;
                     const T amp = a.p.beam ? a.p.beam[long(i) * N + pos] : T(1);
                     const int q = padx<T>(pos);
-                    sre[q] = amp * z.x;
-                    sim[q] = amp * z.y;
+                    const cx<T> h = beam_zero_signs(amp, mk(amp * z.x, amp * z.y));
+                    sre[q] = h.x;
+                    sim[q] = h.y;
                 }
             }
             __syncthreads();
@@ -183,6 +186,8 @@ __global__ void __launch_bounds__(SlabShape<T, N>::THREADS) slab_kernel(SlabArgs
                 slab_fft<T, N, +1>(v, sre, sim, t, smem, a.p.tw_row);
 #pragma unroll
                 for (int r = 0; r < E; ++r) v[r] = v[r] * a.scale;
+            } else if constexpr (mode == SLAB_FWD) {
+                slab_fft<T, N, -1>(v, sre, sim, t, smem, a.p.tw_row);
             } else {   // SLAB_GS, SLAB_FINAL (pass_kernels.cuh COL_GS / COL_FINAL per line)
                 slab_fft<T, N, -1>(v, sre, sim, t, smem, a.p.tw_row);
                 const T gain = a.gain;
@@ -343,21 +348,9 @@ __global__ void __launch_bounds__(256) slab_turn_kernel(const cx<T>* __restrict_
 template <class T, int N, int MODE>
 cudaError_t slab_launch_m(const SlabArgs<T>& a, cudaStream_t st) {
     using Sh = SlabShape<T, N>;
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e =
-            cudaFuncSetAttribute(slab_kernel<T, N, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(Sh::SMEM));
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
-    static int resident = 0;   // persistent grid: CTAs resident at once, capped by the line groups
-    if (!resident) {
-        int dev = 0, sms = 0, per = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, slab_kernel<T, N, MODE>, Sh::THREADS, Sh::SMEM);
-        resident = std::max(1, sms * std::max(1, per));
-    }
+    if (cudaError_t e = ensure_smem_attr<slab_kernel<T, N, MODE>>(Sh::SMEM); e != cudaSuccess) return e;
+    // persistent grid: CTAs resident at once, capped by the line groups
+    const int resident = resident_ctas<slab_kernel<T, N, MODE>>(Sh::THREADS, Sh::SMEM);
     const int grid = std::min(resident, (a.R + Sh::LINES - 1) / Sh::LINES);
     slab_kernel<T, N, MODE><<<grid, Sh::THREADS, Sh::SMEM, st>>>(a);
     return cudaGetLastError();
@@ -372,6 +365,7 @@ cudaError_t slab_launch_n(const SlabArgs<T>& a, int mode, cudaStream_t st) {
         case SLAB_GS: return slab_launch_m<T, N, SLAB_GS>(a, st);
         case SLAB_FINAL: return slab_launch_m<T, N, SLAB_FINAL>(a, st);
         case SLAB_INV: return slab_launch_m<T, N, SLAB_INV>(a, st);
+        case SLAB_FWD: return slab_launch_m<T, N, SLAB_FWD>(a, st);
         default: return cudaErrorInvalidValue;
     }
 }

@@ -118,15 +118,22 @@ def hologram_payload(indices, states, device=None, expand="host"):
         status.append(lib.cgh_hgi_payload(dev, _native.ptr(idx), idx.dtype.itemsize, idx.size, _native.ptr(table),
                                           len(table), out_ptr, ctypes.byref(crc)))
 
-    if expand == "device":
-        out = np.empty(idx.shape, dtype=np.complex128)
-        checksum(_native.ptr(out))
-    else:
-        worker = threading.Thread(target=checksum, args=(None,))
-        worker.start()                                   # the C call releases the GIL
-        out = _native.expand_states(idx, table)
-        worker.join()
-    _native.check(status[0])
+    try:
+        if expand == "device":
+            out = np.empty(idx.shape, dtype=np.complex128)
+            checksum(_native.ptr(out))
+        else:
+            worker = threading.Thread(target=checksum, args=(None,))
+            worker.start()                                   # the C call releases the GIL
+            try:
+                out = _native.expand_states(idx, table)
+            finally:
+                worker.join()
+        _native.check(status[0])
+    except ValueError as exc:
+        if "index outside the state table" in str(exc):   # numpy states[indices]: IndexError
+            raise IndexError(str(exc)) from None
+        raise
     return out, int(crc.value)
 
 

@@ -48,7 +48,7 @@ from .propagation import fill_propagation
 from .runtime import current_device, runner_precision
 from .slm import problem_for, states
 
-SLAB_INIT, SLAB_HOLO, SLAB_GS, SLAB_FINAL, SLAB_INV = 0, 1, 2, 3, 4
+SLAB_INIT, SLAB_HOLO, SLAB_GS, SLAB_FINAL, SLAB_INV, SLAB_FWD = 0, 1, 2, 3, 4, 6
 
 
 def error_from_sums(sdd, srr, srd, denom, rescale):

@@ -49,3 +49,14 @@ def gaussian_beam(h, w, width=0.35):
     y, x = np.mgrid[0:h, 0:w].astype(np.float64)
     r2 = ((x - w / 2) / (width * w)) ** 2 + ((y - h / 2) / (width * h)) ** 2
     return np.exp(-r2).astype(np.complex128)
+
+
+def aperture_beam(h, w, width=0.35, radius=0.4):
+    """Gaussian illumination cut by a circular aperture: exact zeros outside
+    radius * min(h, w) (exercises the zero-amplitude projection, where the
+    reference's complex multiply beam * exp(i angle) yields signed zeros)."""
+    y, x = np.mgrid[0:h, 0:w].astype(np.float64)
+    beam = gaussian_beam(h, w, width)
+    out = ((x - w / 2) ** 2 + (y - h / 2) ** 2) > (radius * min(h, w)) ** 2
+    beam[out] = 0.0
+    return beam

@@ -32,7 +32,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 REPO = os.path.dirname(os.path.dirname(HERE))
 sys.path.insert(0, REPO)
 
-from paper_2006_10509_b200.workloads import gaussian_beam, natural_target, square_target  # noqa: E402
+from paper_2006_10509_b200.workloads import aperture_beam, gaussian_beam, natural_target, square_target  # noqa: E402
 
 REF_COPY = os.environ.get("CGHKIT_BUILD", "/tmp/cghkit_golden_build")
 
@@ -104,6 +104,20 @@ def small_cases(ck):
         seed=7, max_passes=6)
     add("dbs_16_pl4_random_fresnel", "dbs", 16, PhaseOnly(4), square_target(16), target_kind="square",
         prop=fres, mask_rects=[(2, 2, 12, 10)], seed=3, max_passes=4, scan_order="random")
+    # exact-zero illumination (aperture): the reference snaps beam * exp(i angle)
+    # with beam = 0 to the phase of a signed zero (complex multiply by 0 + 0j)
+    add("gs_aperture_32_pl8", "gs", 32, PhaseOnly(8), natural_target(32), illum="aperture", seed=12,
+        iterations=6)
+    add("gs_aperture_32_bin_qeach", "gs", 32, binary_phase(), natural_target(32), illum="aperture",
+        prop=fres, seed=13, iterations=5, quantize_each_iteration=True)
+    add("ospr_aperture_32_bin_4", "ospr", 32, binary_phase(), natural_target(32), illum="aperture",
+        seed=14, subframes=4)
+    add("ospr_aperture_32_pl4_fresnel_3", "ospr", 32, PhaseOnly(4), natural_target(32), illum="aperture",
+        prop=fres, seed=15, subframes=3)
+    add("sa_16_aperture_bin", "sa", 16, binary_phase(), square_target(16), target_kind="square",
+        illum="aperture", seed=16, proposals=600)
+    add("dbs_16_aperture_pl4", "dbs", 16, PhaseOnly(4), square_target(16), target_kind="square",
+        illum="aperture", seed=17, max_passes=3)
     for seed in (1, 2, 3, 4, 5):
         t = np.zeros((2, 2), complex)
         t[1, 1] = 1.0
@@ -175,7 +189,8 @@ def run_case(ck, case, outdir):
         cfgd["metric"] = MetricSpec(rect_mask(128, 64), rescale=False)
     cfg = A.AlgorithmConfig(**cfgd)
     h, w = target.shape
-    illum = gaussian_beam(h, w) if case["illum"] == "beam" else None
+    illum = {"beam": gaussian_beam, "aperture": aperture_beam}.get(case["illum"])
+    illum = None if illum is None else illum(h, w)
     log = []
     cancel = None
     undo = []

@@ -12,7 +12,7 @@ from paper_2006_10509_b200 import algorithms as A
 from paper_2006_10509_b200.image import rect_mask
 from paper_2006_10509_b200.propagation import MetricSpec, PropagationSpec
 from paper_2006_10509_b200.slm import AmplitudeOnly, MultiAmp, PhaseOnly, SlmSpec
-from paper_2006_10509_b200.workloads import gaussian_beam, natural_target, square_target
+from paper_2006_10509_b200.workloads import aperture_beam, gaussian_beam, natural_target, square_target
 
 GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
@@ -55,5 +55,5 @@ def build(rec):
     params = dict(rec["params"])
     cfg = A.AlgorithmConfig(algorithm=rec["algorithm"], slm=SlmSpec(w, h, scheme_from(rec["scheme"])),
                             propagation=prop, metric=MetricSpec(mask, rec["rescale"]), **params)
-    illum = gaussian_beam(h, w) if rec["illumination"] == "beam" else None
-    return cfg, target, illum
+    illum = {"beam": gaussian_beam, "aperture": aperture_beam}.get(rec["illumination"])
+    return cfg, target, None if illum is None else illum(h, w)

@@ -18,6 +18,13 @@ from paper_2006_10509_b200.workloads import gaussian_beam, natural_target
 pytestmark = pytest.mark.gpu
 MAN = G.manifest()["cases"]
 
+# fp32 index-plane mismatches against the reference (decision-boundary pixels),
+# bounded at 2x the count measured on B200 (printed by the tests; round 2:
+# C1 188 of 262144, C3 184 of 4194304, C2 frames 0 and 23: 0)
+C1_FP32_MISMATCH_BOUND = 2 * 188
+C3_FP32_MISMATCH_BOUND = 2 * 184
+C2_FP32_FRAME_BOUND = 2
+
 
 def _field(cfg, target, illum=None, fast=True):
     old = os.environ.pop("CGHB200_NO_FAST", None)
@@ -66,7 +73,9 @@ def test_c1_full_size_fp32_fast_and_fp64():
     assert abs(rep.final_error - rec["final_error"]) / rec["final_error"] < 1e-3
     assert np.max(np.abs(tr - arrs["trace"]) / arrs["trace"]) < 1e-3
     idx = np.argmin(np.abs(holo[..., None] - states(cfg.slm.scheme)[None, None, :]), axis=-1)
-    assert np.mean(idx != arrs["idx0"]) < 1e-3
+    mism = int(np.sum(idx != arrs["idx0"]))
+    print(f"C1 fp32 index mismatches: {mism} / {idx.size}")
+    assert mism <= C1_FP32_MISMATCH_BOUND, mism
     with precision("fp64"):
         holo64, rep64 = A.run_gs(cfg, target)
     assert np.array_equal(holo64, states(cfg.slm.scheme)[arrs["idx0"]])
@@ -88,7 +97,8 @@ def test_c3_full_size_fp32_and_fp64():
     assert np.max(np.abs(tr - arrs["trace"]) / arrs["trace"]) < 1e-3
     idx32 = np.searchsorted(np.angle(table) % (2 * np.pi), np.angle(holo) % (2 * np.pi) - 1e-9)
     mism32 = int(np.sum(holo != table[arrs["idx0"]]))
-    assert mism32 < 4096, mism32           # fp32: boundary pixels only (survey probe: 78 / 4.2M)
+    print(f"C3 fp32 index mismatches: {mism32} / {holo.size}")
+    assert mism32 <= C3_FP32_MISMATCH_BOUND, mism32   # decision-boundary pixels only
     with precision("fp64"):
         holo64, rep64 = A.run_gs(cfg, target)
     mism64 = int(np.sum(holo64 != table[arrs["idx0"]]))
@@ -164,4 +174,6 @@ def test_c2_full_size_fp32_fast():
     assert np.max(np.abs(tr - arrs["trace"]) / arrs["trace"]) < 1e-3
     assert abs(rep.efficiency - rec["efficiency"]) < 1e-4
     for i in (0, len(frames) - 1):
-        assert np.sum(frames[i] != table[arrs[f"idx{i}"]]) <= 64
+        mism = int(np.sum(frames[i] != table[arrs[f"idx{i}"]]))
+        print(f"C2 fp32 frame {i}: {mism} index mismatches")
+        assert mism <= C2_FP32_FRAME_BOUND
