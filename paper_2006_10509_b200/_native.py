@@ -41,7 +41,7 @@ EXPORTS = (
     "cgh_slab_create", "cgh_slab_destroy", "cgh_slab_set_local", "cgh_slab_pass", "cgh_slab_transpose",
     "cgh_slab_turn", "cgh_plan_ospr_part", "cgh_plan_set_intensity", "cgh_plan_intensity",
     "cgh_plan_copy_intensity",
-    "cgh_hgi_payload", "cgh_crc32_combine", "cgh_delta_replay_update",
+    "cgh_hgi_payload", "cgh_crc32_combine", "cgh_delta_replay_update", "cgh_debug_wl_stamps",
 )
 
 
@@ -153,6 +153,7 @@ def _declare(lib):
         "cgh_plan_stream": ([P], P),
         "cgh_plan_sync": ([P], ctypes.c_int),
         "cgh_plan_profile": ([P, i32, P, P, i32], ctypes.c_int),
+        "cgh_debug_wl_stamps": ([P, P, i64], ctypes.c_int),
         "cgh_delta_error": ([i32, P, P, P, P, P, P, i64, i32, i32, f64, f64, pP(f64)], ctypes.c_int),
         "cgh_commit_update": ([i32, P, P, P, P, P, i64, i32, i32, f64, f64], ctypes.c_int),
         "cgh_best_delta": ([i32, P, P, P, P, P, P, i64, i32, i32, P, i64, pP(i64), pP(f64)], ctypes.c_int),

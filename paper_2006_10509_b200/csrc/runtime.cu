@@ -198,6 +198,7 @@ void plan_free(cgh_plan* P) {
     cudaSetDevice(P->dev);
     if (P->st) cudaStreamSynchronize(P->st);
     fast_free(P);
+    wl_free(P);
     cgh::DevBuf* bufs[] = {&P->states64, &P->states32, &P->tw_row, &P->tw_col, &P->q_row, &P->q_col, &P->data,
                            &P->tgt, &P->beam, &P->idx, &P->field, &P->partials, &P->counter, &P->stats, &P->stage,
                            &P->mask, &P->frame_rng, &P->intensity, &P->sa_buf};
@@ -284,6 +285,7 @@ static int prep_target(cgh_plan* P, const double* target, const uint8_t* mask, c
     P->nf_beam = st[4];
     P->target_ready = true;
     fast_invalidate_target(P);
+    wl_invalidate_target(P);
     return CGH_OK;
 }
 
@@ -489,18 +491,48 @@ static int gs_exec(cgh_plan* P, const cgh_gs_params* gp, int64_t* tk, double* tv
         return run_row<T>(P, ROW_HOLO, b, 1);
     };
 
-    bool fast = false;
+    bool fast = false, wlp = false;
     if constexpr (sizeof(T) == 4) {
         fast = fast_eligible(P);
         if (fast) CGH_TRY(fast_prepare(P));
+        // warp-line passes (2048^2): the plane stays column-tiled between the
+        // relayouts; snapping row passes run on the row-major plane
+        wlp = fast && !gp->quantize_each_iteration && wl_eligible(P);
+        if (wlp) CGH_TRY(wl_prepare(P));
     }
+    bool tiled = false;
+    auto to_rowmajor = [&]() -> int {
+        if (tiled) {
+            CGH_TRY(wl_relayout(P, 0));
+            tiled = false;
+        }
+        return CGH_OK;
+    };
     CGH_TRY(run_init(iters == 0 ? 1 : 0));
     ProgressQueue pq;
     const bool has_cancel = cb && cb->cancel, has_progress = cb && cb->progress;
     CGH_TRY(pq.init(P, cb, has_cancel && has_progress ? 0 : (has_cancel ? 4 : 63), P->res_h, 2));
     long executed = 0;
     bool stop = false;
-    for (long k = 0; k < iters; ++k) {
+    long k_first = 0;
+    if constexpr (sizeof(T) == 4) {
+        // no per-iteration host hooks: iterations 0..iters-1 in one persistent
+        // launch; only the last (snapping) hologram-plane pass is left below
+        if (wlp && !has_cancel && !has_progress && iters >= 2 && !getenv("CGHB200_WL_NO_LOOP")) {
+            CGH_TRY(wl_relayout(P, 1));
+            tiled = true;
+            CGH_TRY(wl_gs_loop(P, a, int(iters)));
+            CGH_TRY(to_rowmajor());
+            PassArgs<T> r = a;
+            r.quantize = 1;
+            r.idx_out = P->idx.p;
+            r.field_out = field_dev;
+            CGH_TRY(run_row<T>(P, ROW_HOLO, r, 1));
+            executed = iters;
+            k_first = iters;
+        }
+    }
+    for (long k = k_first; k < iters; ++k) {
         if (cancelled(cb)) {
             stop = true;
             break;
@@ -508,8 +540,17 @@ static int gs_exec(cgh_plan* P, const cgh_gs_params* gp, int64_t* tk, double* tv
         PassArgs<T> c = a;
         c.red.out = P->res_d + 2 * k;
         if constexpr (sizeof(T) == 4) {
-            if (fast) CGH_TRY(fast_col(P, c));
-            else CGH_TRY(run_col<T>(P, COL_GS, c, 1));
+            if (wlp) {
+                if (!tiled) {
+                    CGH_TRY(wl_relayout(P, 1));
+                    tiled = true;
+                }
+                CGH_TRY(wl_col(P, c));
+            } else if (fast) {
+                CGH_TRY(fast_col(P, c));
+            } else {
+                CGH_TRY(run_col<T>(P, COL_GS, c, 1));
+            }
         } else {
             CGH_TRY(run_col<T>(P, COL_GS, c, 1));
         }
@@ -521,15 +562,23 @@ static int gs_exec(cgh_plan* P, const cgh_gs_params* gp, int64_t* tk, double* tv
         r.field_out = last ? field_dev : nullptr;
         bool done_fast = false;
         if constexpr (sizeof(T) == 4) {
-            if (fast && !r.quantize && !r.field_out) {
+            if (wlp && tiled && !r.quantize && !r.field_out) {
+                CGH_TRY(wl_row(P, r));
+                done_fast = true;
+            } else if (fast && !r.quantize && !r.field_out) {
+                CGH_TRY(to_rowmajor());
                 CGH_TRY(fast_row(P, r));
                 done_fast = true;
             }
         }
-        if (!done_fast) CGH_TRY(run_row<T>(P, ROW_HOLO, r, 1));
+        if (!done_fast) {
+            CGH_TRY(to_rowmajor());
+            CGH_TRY(run_row<T>(P, ROW_HOLO, r, 1));
+        }
         executed = k + 1;
         if (has_progress || has_cancel) CGH_TRY(pq.poll(false));
     }
+    CGH_TRY(to_rowmajor());
     if (stop) {
         if (executed == 0) {
             CGH_TRY(run_init(1));

@@ -68,6 +68,7 @@ struct cgh_plan {
     cgh::DevBuf data, tgt, beam, idx, field, partials, counter, stats, stage, mask, frame_rng, intensity;
     cgh::DevBuf sa_buf;   // search state (SA/DBS)
     void* fast = nullptr; // FastState of the pipelined complex64 GS passes (fast.cu)
+    void* wlst = nullptr; // WlState of the warp-line 2048^2 GS passes (wl.cu)
     int idx_bytes = 1;
     bool has_beam = false, target_ready = false;
     // mapped host results
@@ -120,6 +121,16 @@ int fast_row(cgh_plan* P, const PassArgs<float>& a);
 int fast_col(cgh_plan* P, const PassArgs<float>& a);
 void fast_free(cgh_plan* P);
 void fast_invalidate_target(cgh_plan* P);
+// Warp-line complex64 GS passes for 2048 x 2048 planes (wl.cu): the plane is
+// kept column-tiled ("T4") in a buffer of their own between the relayouts.
+bool wl_eligible(cgh_plan* P);
+int wl_prepare(cgh_plan* P);
+int wl_relayout(cgh_plan* P, int to_t4);
+int wl_col(cgh_plan* P, const PassArgs<float>& a);
+int wl_row(cgh_plan* P, const PassArgs<float>& a);
+int wl_gs_loop(cgh_plan* P, const PassArgs<float>& a, int iters);
+void wl_free(cgh_plan* P);
+void wl_invalidate_target(cgh_plan* P);
 bool fast_ospr_eligible(cgh_plan* P);
 int fast_ospr_holo(cgh_plan* P, const PassArgs<float>& a, int frames, int cap, uint8_t* idx_out);
 int fast_ospr_gen(cgh_plan* P, const PassArgs<float>& a);
