@@ -219,7 +219,7 @@ void *cgh_plan_stream(cgh_plan *plan);          /* cudaStream_t of the plan */
 int cgh_plan_profile(cgh_plan *plan, int32_t enable, double *ms, int64_t *counts, int32_t n);
 /* Timing experiments: with profiling on and CGHB200_WL_STAMPS set, the
  * warp-line 2048^2 passes record per-warp stage timestamps (globaltimer,
- * clock64 pairs: [pass 0 row / 1 column][1024 CTAs][14 warps][8 marks][2]). */
+ * clock64 pairs: [pass 0 row / 1 column][1024 CTAs][16 warps][8 marks][2]). */
 int cgh_debug_wl_stamps(cgh_plan *plan, int64_t *out, int64_t cap);
 int cgh_plan_sync(cgh_plan *plan);
 

@@ -121,7 +121,7 @@ static wl::Args wl_args(cgh_plan* P, const PassArgs<float>& a) {
 static int wl_stamp_buf(cgh_plan* P, wl::Args& w, int pass) {
     if (!P->profiling || !getenv("CGHB200_WL_STAMPS")) return CGH_OK;
     WlState* S = wl_state(P);
-    const size_t per = size_t(1024) * wl::LINES * 8 * 2;   // up to 1024 CTAs
+    const size_t per = size_t(1024) * wl::WARPS * 8 * 2;   // up to 1024 CTAs
     CGH_TRY(ensure(P, S->stamps, 2 * per * sizeof(long long)));
     w.stamps = static_cast<long long*>(S->stamps.p) + size_t(pass) * per;
     return CGH_OK;

@@ -40,8 +40,12 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 
 constexpr int N = 2048;
 constexpr int NQUAD = N / 4;              // 4-line groups per pass
-constexpr int LINES = 14;                 // warps (lines) per CTA: 3 quads + 1 pair
-constexpr int THREADS = 32 * LINES;
+constexpr int LINES = 14;                 // line slots per CTA: 3 quads + 1 pair
+// 16 warps: 4 per quad (one line each) and 4 for the pair (two per line, each
+// half a line), so every SM sub-partition (warp w on SMSP w % 4) carries 3.5
+// lines of work
+constexpr int WARPS = 16;
+constexpr int THREADS = 32 * WARPS;
 constexpr size_t LINE_BYTES = size_t(N) * 8;
 // slot g at g * (16 KB + 32 B): the 4 lines of a quad start 32 B apart in the
 // bank space, so the joint stages (4 lines x 8 consecutive points per warp
@@ -52,6 +56,14 @@ constexpr size_t TWB_OFF = size_t(LINES) * SLOT_BYTES;
 constexpr size_t SMEM = TWB_OFF + 15 * 8 * 8;
 
 enum { ROW = 0, COL = 1 };
+
+// Timing experiments only (wrong results), compiled in with -DCGHB200_WL_DEBUG:
+// Args::debug bit 0 skips stages B..B', bit 1 replaces the HBM/L2 traffic.
+#ifdef CGHB200_WL_DEBUG
+constexpr bool kDebug = true;
+#else
+constexpr bool kDebug = false;
+#endif
 
 __device__ __forceinline__ int swz(int i) { return i ^ ((i >> 4) & 15); }
 
@@ -97,7 +109,7 @@ struct Args {
     float scale;               // 1/sqrt(HW)
     double* line_sums;         // COL: [N][3] per-line partial sums
     ReduceArgs red;
-    long long* stamps;         // timing experiments: [grid][LINES][8] globaltimer / clock64 pairs, or nullptr
+    long long* stamps;         // timing experiments: [grid][WARPS][8] globaltimer / clock64 pairs, or nullptr
     int no_stagger;            // timing experiments: both half-CTAs load at once
     int debug;                 // timing experiments (wrong results): 1 = skip stages B..B', 2 = no HBM/L2 traffic
 };
@@ -108,7 +120,7 @@ __device__ __forceinline__ void stamp(const Args& a, int w, int mark) {
     if (a.stamps && (threadIdx.x & 31) == 0) {
         long long g;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
-        long long* p = a.stamps + ((long(blockIdx.x) * LINES + w) * 8 + mark) * 2;
+        long long* p = a.stamps + ((long(blockIdx.x) * WARPS + w) * 8 + mark) * 2;
         p[0] = g;
         p[1] = clock64();
     }
@@ -121,37 +133,48 @@ __device__ __forceinline__ cx<float> twd(cx<float> w) {
     else return conj(w);
 }
 
-// group geometry of warp `w` (0..13): group index, warp within group, size
+// group geometry of warp `w` (0..15). Quads (groups 0..2): warp wi of the
+// group owns line wi. Pair (group 3): warps wi = 2h + sub; sub picks the line,
+// h the half: chunks [2h, 2h + 2) of the joint stages and of stages B / B',
+// [4h, 4h + 4) of stage C (a half line, positions [1024 h, 1024 h + 1024),
+// is self-contained from stage B to B').
 template <int PASS>
 struct Role {
-    int grp, wi, gs;   // group 0..2 quads, 3 pair; warp in group; group size (4 or 2)
+    int grp, wi;       // group 0..2 quads, 3 pair; warp in group (0..3)
     int s, j0;         // joint stages: this thread's line in the group and butterfly base
+    int own;           // slot / line offset in the group of this warp's stages B..B'
+    int h;             // half (pair) or -1 (quad: whole line)
     __device__ Role(int w, int l) {
-        grp = w < 12 ? (w >> 2) : 3;
-        wi = w < 12 ? (w & 3) : (w - 12);
-        gs = w < 12 ? 4 : 2;
-        if (PASS == COL) {
-            if (gs == 4) {
+        grp = w >> 2;
+        wi = w & 3;
+        if (grp < 3) {
+            h = -1;
+            own = wi;
+            if (PASS == COL) {
                 s = l & 3;
                 j0 = 8 * wi + (l >> 2);
             } else {
-                s = l & 1;
-                j0 = 16 * wi + (l >> 1);
-            }
-        } else {
-            if (gs == 4) {
                 s = (l >> 2) & 3;
                 j0 = 8 * wi + 4 * (l >> 4) + (l & 3);
+            }
+        } else {
+            h = wi >> 1;
+            own = wi & 1;
+            if (PASS == COL) {
+                s = l & 1;
+                j0 = 16 * (wi & 1) + (l >> 1);
             } else {
                 s = (l >> 2) & 1;
-                j0 = 16 * wi + 4 * (l >> 3) + (l & 3);
+                j0 = 16 * (wi & 1) + 4 * (l >> 3) + (l & 3);
             }
         }
     }
+    __device__ int a_beg() const { return h < 0 ? 0 : 2 * h; }
+    __device__ int a_cnt() const { return h < 0 ? 4 : 2; }
 };
 
-__device__ __forceinline__ void group_bar(int grp, int gs) {
-    asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(32 * gs) : "memory");
+__device__ __forceinline__ void group_bar(int grp) {
+    asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory");
 }
 
 // first line of this group in round `rb` (quads), or -1 if none
@@ -182,21 +205,26 @@ __device__ __forceinline__ void load_tw(cx<float> (&t)[15], const cx<float>* __r
 template <int PASS, int D>
 __device__ __forceinline__ void load_a(cx<float> (&u)[16], const float2* __restrict__ data, int line, int j,
                                        int dbg = 0) {
-    if (dbg & 2) {
+    if (kDebug && (dbg & 2)) {
 #pragma unroll
         for (int k = 0; k < 16; ++k) u[k] = mk(float(j), float(k));
         return;
     }
     const float2* p = data + t4_line<PASS>(line, j);
-    // ROW: the 16 points are 2 MB apart (beyond the immediate offset range):
-    // step one pointer instead of keeping 16 addresses live
-    long step = kStep128<PASS>;
-    if (PASS == ROW) asm volatile("" : "+l"(step));
+    // ROW: the 16 points are 2 MB apart: four base pointers 8 MB apart keep
+    // every offset inside the immediate range
+    const float2* pb[4];
+    pb[0] = p;
+#pragma unroll
+    for (int q = 1; q < 4; ++q) {
+        long off = 4 * kStep128<PASS>;
+        if (PASS == ROW) asm volatile("" : "+l"(off));
+        pb[q] = pb[q - 1] + off;
+    }
 #pragma unroll
     for (int k = 0; k < 16; ++k) {
-        const float2 z = __ldcg(PASS == ROW ? p : p + k * kStep128<PASS>);
+        const float2 z = __ldcg(PASS == ROW ? pb[k >> 2] + (k & 3) * kStep128<PASS> : p + k * kStep128<PASS>);
         u[k] = mk(z.x, z.y);
-        if (PASS == ROW) p += step;
     }
 }
 
@@ -215,9 +243,9 @@ __device__ __forceinline__ void advance_tw(cx<float> (&twA)[15]) {
 // the line's slot. One code copy for the four chunks (instruction cache).
 template <int PASS, int D>
 __device__ __forceinline__ void stage_a(float2* line_sm, const float2* __restrict__ data, int line, int j0,
-                                        cx<float> (&twA)[15], int dbg) {
+                                        cx<float> (&twA)[15], int dbg, int cbeg, int cend) {
 #pragma unroll 1
-    for (int c = 0; c < 4; ++c) {
+    for (int c = cbeg; c < cend; ++c) {
         const int j = j0 + 32 * c;
         cx<float> u[16];
         load_a<PASS, D>(u, data, line, j, dbg);
@@ -227,7 +255,7 @@ __device__ __forceinline__ void stage_a(float2* line_sm, const float2* __restric
         const SwzA sa(j);
 #pragma unroll
         for (int f = 0; f < 16; ++f) line_sm[sa(f)] = make_float2(u[f].x, u[f].y);
-        advance_tw(twA);
+        if (c + 1 < cend) advance_tw(twA);
     }
 }
 
@@ -237,9 +265,9 @@ __device__ __forceinline__ int k_dummy_line(int line) { return line; }
 // radix 16, store to HBM/L2
 template <int PASS, int D>
 __device__ __forceinline__ void stage_a2(const float2* line_sm, float2* __restrict__ data, int line, int j0,
-                                         cx<float> (&twA)[15], int dbg) {
+                                         cx<float> (&twA)[15], int dbg, int cbeg, int cend) {
 #pragma unroll 1
-    for (int c = 0; c < 4; ++c) {
+    for (int c = cbeg; c < cend; ++c) {
         const int j = j0 + 32 * c;
         cx<float> u[16];
         const SwzA sa(j);
@@ -251,21 +279,26 @@ __device__ __forceinline__ void stage_a2(const float2* line_sm, float2* __restri
 #pragma unroll
         for (int f = 1; f < 16; ++f) u[f] = cmul(u[f], twd<D>(twA[f - 1]));
         Dft<16, D, 1, float>::run(u);
-        advance_tw(twA);
+        if (c + 1 < cend) advance_tw(twA);
         float2* p = data + t4_line<PASS>(line, j);
-        if (dbg & 2) p = data + (threadIdx.x & 31) + 32 * (k_dummy_line(line) & 7);   // timing: one hot line per lane
-        long step = kStep128<PASS>;
-        if (PASS == ROW || (dbg & 2)) asm volatile("" : "+l"(step));
-        if (dbg & 2) step = 0;
+        if (kDebug && (dbg & 2)) {   // timing: arithmetic kept, no stores
 #pragma unroll
-        for (int k = 0; k < 16; ++k) {
-            if (dbg & 2) {
-                if (u[k].x == 1234.5f) __stcg(p, make_float2(u[k].x, u[k].y));   // never true: keeps the arithmetic
-                continue;
-            }
-            __stcg(PASS == ROW ? p : p + k * kStep128<PASS>, make_float2(u[k].x, u[k].y));
-            if (PASS == ROW) p += step;
+            for (int k = 0; k < 16; ++k)
+                if (u[k].x == 1234.5f) __stcg(p, make_float2(u[k].x, u[k].y));
+            continue;
         }
+        float2* pb[4];
+        pb[0] = p;
+#pragma unroll
+        for (int q = 1; q < 4; ++q) {
+            long off = 4 * kStep128<PASS>;
+            if (PASS == ROW) asm volatile("" : "+l"(off));
+            pb[q] = pb[q - 1] + off;
+        }
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+            __stcg(PASS == ROW ? pb[k >> 2] + (k & 3) * kStep128<PASS> : p + k * kStep128<PASS>,
+                   make_float2(u[k].x, u[k].y));
     }
 }
 
@@ -329,10 +362,11 @@ __device__ __forceinline__ void twiddle_b(cx<float> (&u)[16], unsigned tb) {
 
 // FIRST: DIF stage (butterfly, then twiddle); else DIT stage (twiddle, then butterfly)
 template <int D, bool FIRST>
-__device__ __forceinline__ void stage_b_any(float2* line_sm, int lane, unsigned tb) {
+__device__ __forceinline__ void stage_b_any(float2* line_sm, int lane, unsigned tb, int cbeg, int cend) {
     AddrB ad(line_sm, lane);
+    for (int c = 0; c < cbeg; ++c) ad.next();
 #pragma unroll 1
-    for (int c = 0; c < 4; ++c) {
+    for (int c = cbeg; c < cend; ++c) {
         cx<float> u[16];
         ld16_b(u, ad);
         if constexpr (FIRST) Dft<16, D, 1, float>::run(u);
@@ -346,12 +380,12 @@ __device__ __forceinline__ unsigned twb_addr(const float2* wsm, int lane) {
     return saddr(reinterpret_cast<const char*>(wsm) + TWB_OFF) + 8u * unsigned(lane & 7);
 }
 template <int D>
-__device__ __forceinline__ void stage_b(float2* line_sm, int lane, unsigned tb) {
-    stage_b_any<D, true>(line_sm, lane, tb);
+__device__ __forceinline__ void stage_b(float2* line_sm, int lane, unsigned tb, int cbeg, int cend) {
+    stage_b_any<D, true>(line_sm, lane, tb, cbeg, cend);
 }
 template <int D>
-__device__ __forceinline__ void stage_b2(float2* line_sm, int lane, unsigned tb) {
-    stage_b_any<D, false>(line_sm, lane, tb);
+__device__ __forceinline__ void stage_b2(float2* line_sm, int lane, unsigned tb, int cbeg, int cend) {
+    stage_b_any<D, false>(line_sm, lane, tb, cbeg, cend);
 }
 // fill the stage-B table (whole CTA, before the first pass)
 __device__ __forceinline__ void init_twb(float2* wsm, const cx<float>* __restrict__ tw) {
@@ -397,9 +431,10 @@ __device__ __forceinline__ void st8_c(const cx<float> (&u)[8], const AddrC& ad) 
 // ---- stage C (own line): radix 8, projection, radix 8 (second transform)
 template <int PASS, int MODE>
 __device__ __forceinline__ void stage_c_chunks(const Args& a, AddrC& ad, const float* tp, int lane, int myline,
-                                               float& sdd, float& srr, float& srd) {
+                                               float& sdd, float& srr, float& srd, int cbeg, int cend) {
+    for (int C = 0; C < cbeg; ++C) ad.next();
 #pragma unroll 1
-    for (int C = 0; C < 8; ++C) {
+    for (int C = cbeg; C < cend; ++C) {
         constexpr int D1 = PASS == COL ? -1 : +1;
         constexpr int D2 = -D1;
         constexpr bool RESCALE = (MODE & 1) != 0, GAIN = (MODE & 2) != 0;
@@ -478,31 +513,36 @@ __device__ __forceinline__ void pass_body(const Args& a, float2* wsm, double* li
     constexpr bool RESCALE = (MODE & 1) != 0, GAIN = (MODE & 2) != 0;
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const Role<PASS> ro(w, lane);
-    float2* own = slot(wsm, w);
+    const int slot0 = 4 * ro.grp;                 // first slot of the group (pair: 12)
+    float2* own = slot(wsm, slot0 + ro.own);
     float sdd = 0.f, srr = 0.f, srd = 0.f;
+    __shared__ double pair_part[2][3];            // pair, half 1: partial sums per line
+    const int a0 = ro.a_beg(), a1 = a0 + ro.a_cnt();
+    const int b0 = ro.h < 0 ? 0 : 2 * ro.h, b1 = ro.h < 0 ? 4 : b0 + 2;
+    const int c0 = ro.h < 0 ? 0 : 4 * ro.h, c1 = ro.h < 0 ? 8 : c0 + 4;
 
-    // Two half-CTAs run out of phase: the second half (quad 2 + pair) starts
-    // loading its lines only when the first (quads 0, 1) has its lines on
-    // chip, so one half's HBM/L2 traffic overlaps the other's arithmetic.
+    // Optional stagger (CGHB200_WL_STAGGER): the second half-CTA (quad 2 +
+    // pair) starts loading only when the first (quads 0, 1) has its lines on
+    // chip, so one half's memory traffic overlaps the other's arithmetic.
     const bool h2 = ro.grp >= 2;
     for (int rb = 0; rb < NQUAD; rb += round_len()) {
         const int line0 = group_line0(ro.grp, rb);
-        const int line = line0 + ro.s;              // this thread's line in the joint stages
-        float2* gsm = slot(wsm, w - ro.wi + ro.s);  // its slot
-        const int myline = line0 + ro.wi;           // this warp's own line (stages B..B')
+        const int line = line0 + ro.s;            // this thread's line in the joint stages
+        float2* gsm = slot(wsm, slot0 + ro.s);    // its slot
+        const int myline = line0 + ro.own;        // this warp's line in stages B..B'
 
         if (h2 && !a.no_stagger) asm volatile("bar.sync 5, %0;" ::"r"(THREADS) : "memory");
         if (line0 >= 0) {
             cx<float> twA[15];
-            load_tw(twA, a.tw, ro.j0);
-            stage_a<PASS, D1>(gsm, a.data, line, ro.j0, twA, a.debug);
+            load_tw(twA, a.tw, ro.j0 + 32 * a0);
+            stage_a<PASS, D1>(gsm, a.data, line, ro.j0, twA, a.debug, a0, a1);
         }
         if (!h2 && !a.no_stagger) asm volatile("bar.arrive 5, %0;" ::"r"(THREADS) : "memory");
-        if (line0 < 0) continue;   // uniform per group
+        if (line0 < 0) continue;                  // uniform per group
         stamp(a, w, 2);
-        group_bar(ro.grp, ro.gs);
+        group_bar(ro.grp);
         stamp(a, w, 3);
-        if (!(a.debug & 1)) stage_b<D1>(own, lane, twb_addr(wsm, lane));
+        if (!(kDebug && (a.debug & 1))) stage_b<D1>(own, lane, twb_addr(wsm, lane), b0, b1);
         stamp(a, w, 4);
         __syncwarp();
 
@@ -512,34 +552,45 @@ __device__ __forceinline__ void pass_body(const Args& a, float2* wsm, double* li
         else tp = a.beam_perm ? a.beam_perm + long(myline) * N : nullptr;
         {
             AddrC ad(own, lane);
-            if (!(a.debug & 1)) stage_c_chunks<PASS, MODE>(a, ad, tp, lane, myline, sdd, srr, srd);
+            if (!(kDebug && (a.debug & 1)))
+                stage_c_chunks<PASS, MODE>(a, ad, tp, lane, myline, sdd, srr, srd, c0, c1);
         }
         stamp(a, w, 5);
         __syncwarp();
-        if (!(a.debug & 1)) stage_b2<D2>(own, lane, twb_addr(wsm, lane));
+        if (!(kDebug && (a.debug & 1))) stage_b2<D2>(own, lane, twb_addr(wsm, lane), b0, b1);
         stamp(a, w, 6);
+        double s3[3] = {0.0, 0.0, 0.0};
         if constexpr (PASS == COL) {
-            double s3[3] = {double(sdd), double(srr), double(srd)};
+            s3[0] = double(sdd);
+            s3[1] = double(srr);
+            s3[2] = double(srd);
 #pragma unroll
             for (int q = 0; q < 3; ++q)
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) s3[q] += __shfl_xor_sync(0xffffffffu, s3[q], o);
-            if (lane == 0) {
-                const double sc2 = double(a.scale) * double(a.scale);
-                line_sums[3 * long(myline) + 0] = s3[0] * sc2;
-                line_sums[3 * long(myline) + 1] = s3[1] * sc2;
-                line_sums[3 * long(myline) + 2] = s3[2] * sc2;
-            }
+            if (ro.h == 1 && lane == 0)
+#pragma unroll
+                for (int q = 0; q < 3; ++q) pair_part[ro.own][q] = s3[q];
             sdd = srr = srd = 0.f;
         }
-        group_bar(ro.grp, ro.gs);
+        group_bar(ro.grp);
+        if constexpr (PASS == COL) {
+            if (ro.h <= 0 && lane == 0) {   // quad warp, or the pair's first half (+ second, fixed order)
+                const double sc2 = double(a.scale) * double(a.scale);
+#pragma unroll
+                for (int q = 0; q < 3; ++q) {
+                    const double v = ro.h == 0 ? s3[q] + pair_part[ro.own][q] : s3[q];
+                    line_sums[3 * long(myline) + q] = v * sc2;
+                }
+            }
+        }
         {
             cx<float> twA[15];
-            load_tw(twA, a.tw, ro.j0);
-            stage_a2<PASS, D2>(gsm, a.data, line, ro.j0, twA, a.debug);
+            load_tw(twA, a.tw, ro.j0 + 32 * a0);
+            stage_a2<PASS, D2>(gsm, a.data, line, ro.j0, twA, a.debug, a0, a1);
         }
         stamp(a, w, 7);
-        if (rb + round_len() < NQUAD) group_bar(ro.grp, ro.gs);   // the slots are reused by the next round
+        if (rb + round_len() < NQUAD) group_bar(ro.grp);   // the slots are reused by the next round
     }
 }
 

@@ -37,3 +37,6 @@ ti = sum(tot_i.values()); tw = sum(tot_w.values())
 print(f"instructions {ti:.0f}  stall samples {tw:.0f}")
 for k, v in sorted(tot_i.items(), key=lambda x: -x[1])[:35]:
     print(f"{k[0]:>18}:{k[1]:<5} instr {100*v/ti:5.1f}%  stalls {100*tot_w[k]/max(tw,1):5.1f}%")
+print("-- by stall samples")
+for k, v in sorted(tot_w.items(), key=lambda x: -x[1])[:20]:
+    print(f"{k[0]:>18}:{k[1]:<5} instr {100*tot_i[k]/ti:5.1f}%  stalls {100*v/max(tw,1):5.1f}%")

@@ -15,7 +15,7 @@ plan = GenerationPlan(cfg, (n, n), precision=_native.FP32, device=0)
 plan.set_target(natural_target(n))
 for _ in range(2): plan.gs()
 plan.profile(True); plan.gs(); print(plan.profile(False))
-buf = np.zeros(2 * 1024 * 14 * 8 * 2, np.int64)
+buf = np.zeros(2 * 1024 * 16 * 8 * 2, np.int64)
 _native.check(plan.lib.cgh_debug_wl_stamps(plan.handle, _native.ptr(buf), buf.size))
 s = buf[: 8 * 2 * 1024 * 2].reshape(8, 2, 1024, 2)[:, :, :148].astype(np.float64)
 t0 = s[0, 1, :, 0].min()

@@ -16,12 +16,12 @@ plan.set_target(natural_target(n))
 for _ in range(3): plan.gs()
 plan.profile(True); plan.gs(); passes = plan.profile(False)
 print({k: round(1000 * v[0] / max(1, v[1]), 2) for k, v in passes.items()})
-per = 1024 * 14 * 8 * 2
+per = 1024 * 16 * 8 * 2
 buf = np.zeros(2 * per, np.int64)
 _native.check(plan.lib.cgh_debug_wl_stamps(plan.handle, _native.ptr(buf), buf.size))
 names = ["entry", "pdl_wait", "stageA", "barA", "stageB", "stageC", "stageB2", "stageA2"]
 for pas, nm in ((0, "ROW"), (1, "COL")):
-    s = buf[pas * per:(pas + 1) * per].reshape(1024, 14, 8, 2)[:148]
+    s = buf[pas * per:(pas + 1) * per].reshape(1024, 16, 8, 2)[:148]
     g = s[..., 0].astype(np.float64); c = s[..., 1].astype(np.float64)
     t0 = g[:, :, 0].min()
     print(f"{nm}: global timer (us after first entry), min / median / max over warps")
@@ -35,13 +35,13 @@ for pas, nm in ((0, "ROW"), (1, "COL")):
 
 # where the slowest warps are: end of stage A' per warp, by warp slot and CTA
 for pas, nm in ((0, "ROW"), (1, "COL")):
-    s = buf[pas * per:(pas + 1) * per].reshape(1024, 14, 8, 2)[:148]
+    s = buf[pas * per:(pas + 1) * per].reshape(1024, 16, 8, 2)[:148]
     g = s[..., 0].astype(np.float64)
     t0 = g[:, :, 0][g[:, :, 0] > 0].min()
     end = (g[:, :, 7] - t0) / 1000
     start = (g[:, :, 1] - t0) / 1000
     valid = g[:, :, 7] > 0
-    print(f"{nm}: end of pass by warp slot (median over CTAs):", np.round([np.median(end[:, w][valid[:, w]]) for w in range(14)], 2))
+    print(f"{nm}: end of pass by warp slot (median over CTAs):", np.round([np.median(end[:, w][valid[:, w]]) for w in range(16)], 2))
     ce = np.where(valid, end, 0).max(axis=1)
     print(f"{nm}: per-CTA end: min {ce.min():.2f} median {np.median(ce):.2f} max {ce.max():.2f}; slowest CTAs", np.argsort(ce)[-8:], np.round(np.sort(ce)[-8:], 2))
     print(f"{nm}: per-CTA start (pdl_wait) max {start.max():.2f}")
