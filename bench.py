@@ -150,7 +150,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:  # noqa: BLE001
             self.proc = None
         return self
@@ -331,7 +331,11 @@ def run_ours(args):
     hw = N_PX * N_PX
     peak, peak_src = peaks()
     cand = []
-    for name, bpp in (("col_gs", COL_BYTES_PER_PX), ("row_holo", ROW_BYTES_PER_PX)):
+    # the persistent warp-line loop (wl_loop: ITERS replay-plane passes at 20
+    # B/px and ITERS - 1 hologram-plane passes at 16 B/px in one launch) when
+    # it ran, else the per-pass kernels
+    loop_bpp = (COL_BYTES_PER_PX * ITERS + ROW_BYTES_PER_PX * (ITERS - 1))
+    for name, bpp in (("gs_loop", loop_bpp), ("col_gs", COL_BYTES_PER_PX), ("row_holo", ROW_BYTES_PER_PX)):
         ms, cnt = passes.get(name, (0.0, 0))
         if cnt:
             avg = ms / cnt
@@ -348,7 +352,9 @@ def run_ours(args):
     roofline = None
     if cand:
         _, name, achieved, avg_ms, bpp = cand[0]
-        roofline = {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": peak, "unit": "GB/s",
+        kname = {"gs_loop": "wl_loop (persistent GS loop: 200 replay-plane + 199 hologram-plane passes per launch)",
+                 "col_gs": "column pass", "row_holo": "row pass"}.get(name, name)
+        roofline = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak, "unit": "GB/s",
                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                     "algorithmic_bytes_per_launch": bpp * hw, "avg_launch_ms": avg_ms,
                     "per_iteration": {"bytes": GS_BYTES_PER_PX * hw, "ms": iter_ms,
