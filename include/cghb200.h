@@ -186,6 +186,15 @@ typedef struct cgh_plan cgh_plan;
 int cgh_plan_create(const cgh_problem *pb, cgh_plan **out);
 int cgh_plan_destroy(cgh_plan *plan);
 int cgh_plan_set_target(cgh_plan *plan, const double *target, const uint8_t *mask, const double *illumination);
+/* As cgh_plan_set_target; flags bit 0 (CGH_TARGET_AMPLITUDE_ONLY): the runs of
+ * this target never start from the backpropagated target (random-phase GS /
+ * SA / DBS, OSPR), so fp32 plans build the shifted amplitude plane on host
+ * threads and upload 4 B/px instead of the complex128 target and the mask. A
+ * backpropagation start then fails with CGH_ERR_VALUE until the target is set
+ * again with flags = 0. */
+#define CGH_TARGET_AMPLITUDE_ONLY 1
+int cgh_plan_set_target_ex(cgh_plan *plan, const double *target, const uint8_t *mask, const double *illumination,
+                           int32_t flags);
 int cgh_plan_gs(cgh_plan *plan, const cgh_gs_params *gp, int64_t *trace_k, double *trace_v, int64_t trace_cap,
                 cgh_report *rep, const cgh_callbacks *cb);
 int cgh_plan_ospr(cgh_plan *plan, const cgh_ospr_params *op, int64_t *trace_k, double *trace_v,

@@ -33,7 +33,8 @@ INIT_RANDOM, INIT_BACKPROP = 0, 1
 EXPORTS = (
     "cgh_version", "cgh_last_error", "cgh_device_count", "cgh_transform", "cgh_masked_sums", "cgh_quantize",
     "cgh_gs_run", "cgh_ospr_run", "cgh_sa_run", "cgh_dbs_run",
-    "cgh_plan_create", "cgh_plan_destroy", "cgh_plan_set_target", "cgh_plan_gs", "cgh_plan_ospr",
+    "cgh_plan_create", "cgh_plan_destroy", "cgh_plan_set_target", "cgh_plan_set_target_ex", "cgh_plan_gs",
+    "cgh_plan_ospr",
     "cgh_plan_sa", "cgh_plan_dbs",
     "cgh_plan_download_idx", "cgh_plan_stream", "cgh_plan_sync", "cgh_plan_profile",
     "cgh_delta_error", "cgh_commit_update", "cgh_best_delta",
@@ -145,6 +146,7 @@ def _declare(lib):
         "cgh_plan_create": ([pP(Problem), pP(P)], ctypes.c_int),
         "cgh_plan_destroy": ([P], ctypes.c_int),
         "cgh_plan_set_target": ([P, P, P, P], ctypes.c_int),
+        "cgh_plan_set_target_ex": ([P, P, P, P, i32], ctypes.c_int),
         "cgh_plan_gs": ([P, pP(GsParams), P, P, i64, pP(Report), pP(Callbacks)], ctypes.c_int),
         "cgh_plan_ospr": ([P, pP(OsprParams), P, P, i64, pP(Report), pP(Callbacks)], ctypes.c_int),
         "cgh_plan_download_idx": ([P, P, i64], ctypes.c_int),

@@ -252,7 +252,7 @@ def run_gs(cfg, target, illumination=None, progress=None, cancel=None):
     _native.library()
     _native.require_device()
     plan = _cached_plan(cfg, target.shape)
-    plan.set_target(target, illumination, cfg=cfg)
+    plan.set_target(target, illumination, cfg=cfg, amplitude_only=cfg.init_mode == RANDOM_PHASE)
     hooks = _Hooks(progress, cancel) if (progress is not None or cancel is not None) else None
     out = _native.PrefaultedArrays(target.shape)    # faulted in while the device iterates
     rep, (tk, tv) = plan.gs(cfg=cfg, hooks=hooks)
@@ -308,7 +308,7 @@ def run_ospr(cfg, target, illumination=None, progress=None, cancel=None):
     _native.library()
     _native.require_device()
     plan = _cached_plan(cfg, target.shape)
-    plan.set_target(target, illumination, cfg=cfg)
+    plan.set_target(target, illumination, cfg=cfg, amplitude_only=True)   # OSPR never backpropagates
     hooks = _Hooks(progress, cancel) if (progress is not None or cancel is not None) else None
     out = _native.PrefaultedArrays(target.shape, max(0, int(cfg.subframes)))
     rep, (tk, tv) = plan.ospr(cfg=cfg, hooks=hooks)

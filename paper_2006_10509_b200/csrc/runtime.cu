@@ -207,6 +207,9 @@ void plan_free(cgh_plan* P) {
     if (P->st) cudaStreamSynchronize(P->st);
     if (P->res_h) cudaFreeHost(P->res_h);
     for (void* h : P->pin) cudaFreeHost(h);
+    if (P->pin_amp) cudaFreeHost(P->pin_amp);
+    for (auto s : P->amp_st) cudaStreamDestroy(s);
+    for (auto e : P->amp_ev) cudaEventDestroy(e);
     for (auto st : P->pin_st) cudaStreamDestroy(st);
     for (auto e : P->pin_ev) cudaEventDestroy(e);
     for (auto e : P->evpool) cudaEventDestroy(e);
@@ -264,6 +267,7 @@ static int prep_target(cgh_plan* P, const double* target, const uint8_t* mask, c
         CGH_TRY(upload_staged(P, ic, illum, size_t(n) * 16));
     }
     P->has_beam = illum != nullptr;
+    P->stage_valid = true;
     const int grid = grid_for(n);
     CGH_TRY(ensure(P, P->partials, size_t(grid) * 5 * sizeof(double)));
     PrepStats ps;
@@ -350,6 +354,143 @@ int upload_staged(cgh_plan* P, void* dst, const void* src, size_t bytes) {
     // pinned chunks are reused by the next upload only after these DMAs: the
     // next call records `start` on P->st, which now waits for them
     return CGH_OK;
+}
+
+// fp32 plans whose runs never start from the backpropagated target: the
+// shifted, mask-signed amplitude plane (prep_kernel's output) and the beam
+// amplitude are built by host threads straight into pinned memory and copied
+// in row chunks as they are produced: 4 B/px cross PCIe instead of the 16 B/px
+// complex128 target plus the mask. Statistics in fp64, fixed order per thread
+// and across threads.
+static int prep_target_host_f32(cgh_plan* P, const double* target, const uint8_t* mask, const double* illum) {
+    const int H = P->H, W = P->W;
+    const long n = long(H) * W;
+    const size_t plane = size_t(n) * sizeof(float);
+    const size_t need = plane * (illum ? 2 : 1);
+    const char* ntenv = getenv("CGHB200_PREP_THREADS");
+    const int nt = ntenv ? std::max(1, std::min(64, atoi(ntenv)))
+                         : std::max(1, std::min(16, int(std::thread::hardware_concurrency())));
+    if (int(P->amp_st.size()) < nt) {
+        while (int(P->amp_st.size()) < nt) {
+            cudaStream_t st;
+            CGH_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+            P->amp_st.push_back(st);
+            cudaEvent_t e;
+            CGH_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            P->amp_ev.push_back(e);
+        }
+    }
+    for (auto st : P->amp_st) CGH_CUDA(cudaStreamSynchronize(st));   // earlier copies out of pin_amp done
+    if (P->pin_amp_cap < need) {
+        if (P->pin_amp) CGH_CUDA(cudaFreeHost(P->pin_amp));
+        P->pin_amp = nullptr;
+        P->pin_amp_cap = 0;
+        CGH_CUDA(cudaHostAlloc(&P->pin_amp, need, cudaHostAllocDefault));
+        P->pin_amp_cap = need;
+    }
+    CGH_TRY(ensure(P, P->tgt, plane));
+    if (illum) CGH_TRY(ensure(P, P->beam, plane));
+    P->has_beam = illum != nullptr;
+    // the device buffers may still be read by earlier work on P->st
+    cudaEvent_t start = P->amp_ev[0];
+    CGH_CUDA(cudaEventRecord(start, P->st));
+    for (int t = 0; t < nt; ++t) CGH_CUDA(cudaStreamWaitEvent(P->amp_st[t], start, 0));
+    float* amp = static_cast<float*>(P->pin_amp);
+    float* bamp = illum ? amp + n : nullptr;
+    std::vector<double> st(size_t(nt) * 5, 0.0);
+    std::atomic<int> err{0};
+    auto mag = [](double re, double im) {
+        const double t = std::sqrt(re * re + im * im);
+        // overflow / underflow of the squares, non-finite input: as hypot
+        if (!(t < 1e150) || t < 1e-150) return std::hypot(re, im);
+        return t;
+    };
+    auto worker = [&](int t) {
+        cudaSetDevice(P->dev);
+        const int u0 = int(long(H) * t / nt), u1 = int(long(H) * (t + 1) / nt);
+        const int rows_per_copy = std::max(1, int((size_t(256) << 10) / (size_t(W) * sizeof(float))));
+        double cnt = 0, den = 0, nfm = 0, nfa = 0, nfb = 0;
+        int flushed = u0;
+        for (int u = u0; u < u1; ++u) {
+            const int uc = u + H / 2 >= H ? u + H / 2 - H : u + H / 2;
+            const double* trow = target + 2 * long(uc) * W;
+            const uint8_t* mrow = mask + long(uc) * W;
+            float* orow = amp + long(u) * W;
+            for (int v = 0; v < W; ++v) {
+                const int vc = v + W / 2 >= W ? v + W / 2 - W : v + W / 2;
+                const double re = trow[2 * vc], im = trow[2 * vc + 1];
+                const double a = mag(re, im);
+                const bool in = mrow[vc] != 0;
+                const bool fin = std::isfinite(re) && std::isfinite(im);
+                if (in) {
+                    cnt += 1.0;
+                    den += a * a;
+                    if (!fin) nfm += 1.0;
+                }
+                if (!fin) nfa += 1.0;
+                const float af = float(a);
+                orow[v] = in ? af : -af;   // -0.0 for dark pixels outside the mask
+            }
+            if (bamp) {   // the beam is not shifted (hologram plane)
+                const double* irow = illum + 2 * long(u) * W;
+                float* brow = bamp + long(u) * W;
+                for (int v = 0; v < W; ++v) {
+                    const double br = irow[2 * v], bi = irow[2 * v + 1];
+                    if (!(std::isfinite(br) && std::isfinite(bi))) nfb += 1.0;
+                    brow[v] = float(mag(br, bi));
+                }
+            }
+            if (u + 1 - flushed >= rows_per_copy || u + 1 == u1) {
+                const size_t off = size_t(flushed) * W, len = size_t(u + 1 - flushed) * W * sizeof(float);
+                if (cudaMemcpyAsync(static_cast<float*>(P->tgt.p) + off, amp + off, len, cudaMemcpyHostToDevice,
+                                    P->amp_st[t]) != cudaSuccess)
+                    err = 1;
+                if (bamp && cudaMemcpyAsync(static_cast<float*>(P->beam.p) + off, bamp + off, len,
+                                            cudaMemcpyHostToDevice, P->amp_st[t]) != cudaSuccess)
+                    err = 1;
+                flushed = u + 1;
+            }
+        }
+        double* s = &st[size_t(t) * 5];
+        s[0] = cnt;
+        s[1] = den;
+        s[2] = nfm;
+        s[3] = nfa;
+        s[4] = nfb;
+    };
+    std::vector<std::thread> th;
+    for (int t = 1; t < nt; ++t) th.emplace_back(worker, t);
+    worker(0);
+    for (auto& x : th) x.join();
+    if (err) return fail(CGH_ERR_CUDA, "amplitude upload failed");
+    for (int t = 0; t < nt; ++t) {
+        CGH_CUDA(cudaEventRecord(P->amp_ev[t], P->amp_st[t]));
+        CGH_CUDA(cudaStreamWaitEvent(P->st, P->amp_ev[t], 0));
+    }
+    double tot[5] = {0, 0, 0, 0, 0};
+    for (int t = 0; t < nt; ++t)
+        for (int q = 0; q < 5; ++q) tot[q] += st[size_t(t) * 5 + q];
+    P->count_in = tot[0];
+    P->denom = tot[1];
+    P->nf_in = tot[2];
+    P->nf_all = tot[3];
+    P->nf_beam = tot[4];
+    // the denominator is read on the device (ReduceArgs::denom -> stats[1])
+    double dev_stats[5] = {tot[0], tot[1], tot[2], tot[3], tot[4]};
+    CGH_CUDA(cudaMemcpyAsync(P->stats.p, dev_stats, sizeof(dev_stats), cudaMemcpyHostToDevice, P->st));
+    CGH_CUDA(cudaStreamSynchronize(P->st));   // dev_stats is a temporary
+    P->target_ready = true;
+    P->stage_valid = false;
+    fast_invalidate_target(P);
+    wl_invalidate_target(P);
+    return CGH_OK;
+}
+
+int plan_upload_target_ex(cgh_plan* P, const double* target, const uint8_t* mask, const double* illum, int flags) {
+    if (!target || !mask) return fail(CGH_ERR_VALUE, "target and mask are required");
+    CGH_CUDA(cudaSetDevice(P->dev));
+    if ((flags & 1) && P->prec == CGH_FP32) return prep_target_host_f32(P, target, mask, illum);
+    return P->prec == CGH_FP64 ? prep_target<double>(P, target, mask, illum) : prep_target<float>(P, target, mask, illum);
 }
 
 int plan_upload_target(cgh_plan* P, const double* target, const uint8_t* mask, const double* illum) {
@@ -483,6 +624,8 @@ static int gs_exec(cgh_plan* P, const cgh_gs_params* gp, int64_t* tk, double* tv
         b.field_out = quantize ? field_dev : nullptr;
         if (gp->init_mode == CGH_INIT_RANDOM_PHASE) return run_row<T>(P, ROW_INIT, b, 1);
         // backpropagate: ifftshift(T) -> inverse columns -> ROW_HOLO (rows + projection)
+        if (!P->stage_valid)
+            return fail(CGH_ERR_VALUE, "backpropagation start needs the complex target (cgh_plan_set_target)");
         load_field_kernel<T><<<grid_for(n), 256, 0, P->st>>>(static_cast<const double*>(P->stage.p), b.data, P->H, P->W, 1,
                                                              nullptr, nullptr, static_cast<unsigned*>(P->counter.p) + 8);
         P->launches += 1;
@@ -1013,6 +1156,12 @@ int cgh_plan_destroy(cgh_plan* plan) {
 int cgh_plan_set_target(cgh_plan* plan, const double* target, const uint8_t* mask, const double* illumination) {
     if (!plan) return fail(CGH_ERR_VALUE, "null plan");
     return plan_upload_target(plan, target, mask, illumination);
+}
+
+int cgh_plan_set_target_ex(cgh_plan* plan, const double* target, const uint8_t* mask, const double* illumination,
+                           int32_t flags) {
+    if (!plan) return fail(CGH_ERR_VALUE, "null plan");
+    return plan_upload_target_ex(plan, target, mask, illumination, flags);
 }
 
 int cgh_plan_gs(cgh_plan* plan, const cgh_gs_params* gp, int64_t* trace_k, double* trace_v, int64_t trace_cap,

@@ -77,6 +77,13 @@ struct cgh_plan {
     std::vector<void*> pin;
     std::vector<cudaStream_t> pin_st;
     std::vector<cudaEvent_t> pin_ev;
+    // host-side amplitude preparation (cgh_plan_set_target_ex, fp32): pinned
+    // plane, one stream per host thread
+    void* pin_amp = nullptr;
+    size_t pin_amp_cap = 0;
+    std::vector<cudaStream_t> amp_st;
+    std::vector<cudaEvent_t> amp_ev;
+    bool stage_valid = false;   // the complex target is on the device (P->stage)
     double* res_d = nullptr;
     size_t res_cap = 0;
     // prep statistics

@@ -645,6 +645,8 @@ static int search_setup(SearchRun& S, int init_mode, const cgh_pcg64& rng0, bool
     if (init_mode == CGH_INIT_RANDOM_PHASE) {
         CGH_TRY(run_row<double>(P, ROW_INIT, a, 1));
     } else {
+        if (!P->stage_valid)
+            return fail(CGH_ERR_VALUE, "backpropagation start needs the complex target (cgh_plan_set_target)");
         load_field_kernel<double><<<grid_for(n), 256, 0, P->st>>>(static_cast<const double*>(P->stage.p), a.data, P->H,
                                                                   P->W, 1, nullptr, nullptr,
                                                                   static_cast<unsigned*>(P->counter.p) + 8);

@@ -203,7 +203,7 @@ class OsprShardSession:
         self._xcache = {}
         for _ in self.rank_ids:
             p = GenerationPlan(cfg, target.shape, precision=precision, device=device)
-            p.set_target(target, illumination)
+            p.set_target(target, illumination, amplitude_only=True)   # OSPR: no backpropagation start
             self.plans.append(p)
 
     def run(self, seed=None):

@@ -57,12 +57,15 @@ class GenerationPlan:
         except Exception:  # noqa: BLE001
             pass
 
-    def set_target(self, target, illumination=None, cfg=None):
+    def set_target(self, target, illumination=None, cfg=None, amplitude_only=False):
+        """Upload a target. ``amplitude_only``: the runs will not start from the
+        backpropagated target (fp32 plans then upload only the shifted,
+        mask-signed amplitude, built by host threads)."""
         target = _native.c128(target)
         mask = _mask_bytes(cfg or self.cfg, target)
         ill = None if illumination is None else _native.c128(illumination)
-        _native.check(self.lib.cgh_plan_set_target(self.handle, _native.ptr(target), _native.ptr(mask),
-                                                   _native.ptr(ill)))
+        _native.check(self.lib.cgh_plan_set_target_ex(self.handle, _native.ptr(target), _native.ptr(mask),
+                                                      _native.ptr(ill), 1 if amplitude_only else 0))
 
     def gs(self, seed=None, iterations=None, with_trace=True, cfg=None, hooks=None):
         cfg = cfg or self.cfg

@@ -13,8 +13,9 @@ not correctly rounded on 35%), so the reference's outcome there depends on the
 host CPU. Such values (the constructed half-way phases exp(i (k + 1/2) 2 pi / L)
 and distance ties such as -1j for MultiAmp((0.2+0.1j, -0.5, 1j, 0.9))) must map
 to one of their two candidates and are counted; every other value is bit-exact.
-Exact ties that the reference's formula sees as exact (remainder == 0.5, equal
-distances) are bit-exact, including the reference tests' own tie cases."""
+The reference tests' own tie cases (exp(i pi/2) for binary, exp(-i pi/4) for
+L = 4, MultiAmp((0, 1)) at 0.5) are checked bit-exactly in
+test_device_quantize_known_answers."""
 
 import os
 
@@ -38,7 +39,7 @@ def _near_tie(vals, scheme):
         frac = np.mod((np.angle(vals) - scheme.phase_offset) / (2.0 * np.pi / L), L)
         rem = frac - np.floor(frac)
         lo = np.floor(frac).astype(np.int64) % L
-        near = (np.abs(rem - 0.5) < 1e-9) & (rem != 0.5)
+        near = np.abs(rem - 0.5) < 1e-9   # includes ties that are exact only in this host's numpy atan2
         return near, np.stack([lo, (lo + 1) % L, (lo + 1) % L])
     d = np.abs(vals[:, None] - table[None, :])
     order = np.argsort(d, axis=1, kind="stable")
