@@ -523,12 +523,18 @@ def run_ours(args):
         exch_kind = "none (G = 1: local block transposes)"
         sess = None
         if world > 1 or FORCE_DIST:
-            try:   # NVLink peer stores from the fused turn kernel (torch symmetric memory)
-                sess = SL.SlabSession(c6cfg, target6, exchange=SL.SymmetricExchange(), precision=_native.FP32,
+            try:   # the library's data plane: IPC peer stores from the fused turn kernel + device barrier, NCCL sums
+                sess = SL.SlabSession(c6cfg, target6, exchange=SL.NcclExchange(device=local), precision=_native.FP32,
                                       device=local)
-                exch_kind = "fused turn kernel: transposed blocks stored to peer buffers over NVLink + device barrier"
+                exch_kind = ("fused turn kernel: transposed blocks stored to CUDA-IPC-mapped peer buffers over NVLink "
+                             "+ device barrier on peer flags (cgh_multi_*)")
             except Exception as exc:  # noqa: BLE001
-                exch_kind = f"nccl all_to_all_single (symmetric memory unavailable: {type(exc).__name__}: {exc})"
+                try:   # torch symmetric memory for the peer mappings
+                    sess = SL.SlabSession(c6cfg, target6, exchange=SL.SymmetricExchange(), precision=_native.FP32,
+                                          device=local)
+                    exch_kind = f"fused turn kernel over torch symmetric memory (cgh_multi unavailable: {exc})"
+                except Exception as exc2:  # noqa: BLE001
+                    exch_kind = f"nccl all_to_all_single (peer mappings unavailable: {type(exc2).__name__}: {exc2})"
             if world > 1:   # every rank takes the same exchange
                 ok = torch.tensor([1 if sess is not None else 0], dtype=torch.int32, device=f"cuda:{local}")
                 dist.all_reduce(ok, op=dist.ReduceOp.MIN)
@@ -553,6 +559,8 @@ def run_ours(args):
         t6 = max_over_ranks(sum(c6ms)) / 1000.0
         err6 = sess.errors(sums6, done6)
         sess.close()
+        if hasattr(sess.exch, "close"):
+            sess.exch.close()
         hw6 = C6_N * C6_N
         ms6 = max_over_ranks(sum(c6ms)) / len(c6ms) / C6_ITERS
         c6 = {"metric": f"distributed GS iterations/s ({C6_N}x{C6_N} Fourier PhaseOnly(8), one plane over "
@@ -583,10 +591,15 @@ def run_ours(args):
         kind2 = "none (1 GPU)"
         exch2 = None
         if world > 1 or FORCE_DIST:
+            from paper_2006_10509_b200.slab import NcclExchange
+
             try:
-                exch2, kind2 = SymmetricExchange(), "|R|^2 totals read through NVLink peer pointers"
+                exch2, kind2 = NcclExchange(device=local), "library NCCL all-gather of |R|^2 totals (cgh_multi_*)"
             except Exception:  # noqa: BLE001
-                exch2, kind2 = TorchExchange(), "NCCL all-gather of |R|^2 totals"
+                try:
+                    exch2, kind2 = SymmetricExchange(), "|R|^2 totals read through NVLink peer pointers"
+                except Exception:  # noqa: BLE001
+                    exch2, kind2 = TorchExchange(), "NCCL all-gather of |R|^2 totals"
         with device(local), precision("fp32"):
             sess2 = OsprShardSession(scfg2, t2, exchange=exch2)
             sess2.run()                                                            # warm
@@ -598,6 +611,8 @@ def run_ours(args):
             barrier()
             ts2 = max_over_ranks(time.perf_counter() - t0) / reps2
             sess2.close()
+            if exch2 is not None and hasattr(exch2, "close"):
+                exch2.close()
         ospr_sh = {"metric": f"OSPR holograms/s, one C2 hologram ({OSPR_N}x{OSPR_N} binary, {OSPR_S} subframes) "
                              f"sharded over {world} GPU(s)", "value": 1.0 / ts2, "unit": "holograms/s",
                    "scaling": "strong", "exchange": kind2,

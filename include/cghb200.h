@@ -275,6 +275,33 @@ int cgh_slab_transpose(cgh_slab *slab, const void *src, void *dst);
  * next reads after it with a device barrier (one per turn). */
 int cgh_slab_turn(cgh_slab *slab, const void *src, void *const *dst_blocks);
 
+/* ---- multi-GPU plumbing (one process per GPU; SURVEY.md §8(b) cgh_multi_*,
+ * §8(e)): NCCL communicators (NCCL resolved at run time from the process's
+ * libnccl.so.2), CUDA IPC peer mappings and a device barrier on peer flags.
+ * Used by the distributed modes for the C6 corner turn (fused peer-store turn
+ * cgh_slab_turn + cgh_multi_device_barrier, or cgh_multi_all_to_all), the
+ * all-reduce of error sums and the all-gather of OSPR |R|^2 totals.
+ * Replaces the torch.distributed data plane of the round-1 drivers; torch
+ * only bootstraps (broadcast of the 128-byte id, exchange of IPC handles). */
+typedef struct cgh_multi cgh_multi;
+int cgh_multi_available(void);                 /* 1 when NCCL could be resolved */
+int cgh_multi_unique_id(uint8_t *out128);      /* rank 0: ncclGetUniqueId */
+int cgh_multi_create(int32_t device, int32_t world, int32_t rank, const uint8_t *id128, void *stream,
+                     cgh_multi **out);         /* ncclCommInitRank; stream NULL = own stream */
+int cgh_multi_destroy(cgh_multi *m);
+/* block g (bytes_per_peer) of send -> rank g, block g of recv <- rank g */
+int cgh_multi_all_to_all(cgh_multi *m, const void *send, void *recv, int64_t bytes_per_peer, void *stream);
+int cgh_multi_all_reduce_sum_f64(cgh_multi *m, double *buf, int64_t count, void *stream);
+int cgh_multi_all_gather(cgh_multi *m, const void *send, void *recv, int64_t bytes, void *stream);
+int cgh_multi_ipc_handle(cgh_multi *m, void *ptr, uint8_t *out64);
+int cgh_multi_ipc_open(cgh_multi *m, const uint8_t *handle64, void **out);
+int cgh_multi_flags(cgh_multi *m, void **out);
+int cgh_multi_set_peer_flags(cgh_multi *m, void *const *flags);
+int cgh_multi_device_barrier(cgh_multi *m, void *stream);
+/* cudaMalloc / cudaFree on a device (IPC-exportable allocation bases) */
+int cgh_device_alloc(int32_t device, int64_t bytes, void **out);
+int cgh_device_free(int32_t device, void *ptr);
+
 /* ---- .hgi payload (cghkit/serialio.py:167-185 save_field): the complex128
  * payload states[idx] of an index plane, expanded on the device and copied to
  * out_payload (count x 16 bytes, may be NULL), and zlib's CRC-32 of those

@@ -43,6 +43,9 @@ EXPORTS = (
     "cgh_slab_turn", "cgh_plan_ospr_part", "cgh_plan_set_intensity", "cgh_plan_intensity",
     "cgh_plan_copy_intensity",
     "cgh_hgi_payload", "cgh_crc32_combine", "cgh_delta_replay_update", "cgh_debug_wl_stamps",
+    "cgh_multi_available", "cgh_multi_unique_id", "cgh_multi_create", "cgh_multi_destroy", "cgh_multi_all_to_all",
+    "cgh_multi_all_reduce_sum_f64", "cgh_multi_all_gather", "cgh_multi_ipc_handle", "cgh_multi_ipc_open",
+    "cgh_multi_flags", "cgh_multi_set_peer_flags", "cgh_multi_device_barrier", "cgh_device_alloc", "cgh_device_free",
 )
 
 
@@ -156,6 +159,20 @@ def _declare(lib):
         "cgh_plan_sync": ([P], ctypes.c_int),
         "cgh_plan_profile": ([P, i32, P, P, i32], ctypes.c_int),
         "cgh_debug_wl_stamps": ([P, P, i64], ctypes.c_int),
+        "cgh_multi_available": ([], ctypes.c_int),
+        "cgh_multi_unique_id": ([P], ctypes.c_int),
+        "cgh_multi_create": ([i32, i32, i32, P, P, pP(P)], ctypes.c_int),
+        "cgh_multi_destroy": ([P], ctypes.c_int),
+        "cgh_multi_all_to_all": ([P, P, P, i64, P], ctypes.c_int),
+        "cgh_multi_all_reduce_sum_f64": ([P, P, i64, P], ctypes.c_int),
+        "cgh_multi_all_gather": ([P, P, P, i64, P], ctypes.c_int),
+        "cgh_multi_ipc_handle": ([P, P, P], ctypes.c_int),
+        "cgh_multi_ipc_open": ([P, P, pP(P)], ctypes.c_int),
+        "cgh_multi_flags": ([P, pP(P)], ctypes.c_int),
+        "cgh_multi_set_peer_flags": ([P, P], ctypes.c_int),
+        "cgh_multi_device_barrier": ([P, P], ctypes.c_int),
+        "cgh_device_alloc": ([i32, i64, pP(P)], ctypes.c_int),
+        "cgh_device_free": ([i32, P], ctypes.c_int),
         "cgh_delta_error": ([i32, P, P, P, P, P, P, i64, i32, i32, f64, f64, pP(f64)], ctypes.c_int),
         "cgh_commit_update": ([i32, P, P, P, P, P, i64, i32, i32, f64, f64], ctypes.c_int),
         "cgh_best_delta": ([i32, P, P, P, P, P, P, i64, i32, i32, P, i64, pP(i64), pP(f64)], ctypes.c_int),

@@ -137,8 +137,21 @@ def _ospr_plane_exchange(plans, exch, rank_ids, world, cache=None):
     into a (G, H, W) tensor and sum its first rank planes on the device."""
     import torch
 
-    from .slab import SimulatedExchange, SymmetricExchange, TorchExchange
+    from .slab import NcclExchange, SimulatedExchange, SymmetricExchange, TorchExchange
 
+    if isinstance(exch, NcclExchange):   # the library's NCCL all-gather on the pass stream
+        (p,) = plans
+        rank = rank_ids[0]
+        n_el = p.shape[0] * p.shape[1]
+        dt = torch.float64 if p.pb.precision == 1 else torch.float32
+        dev = torch.device("cuda", p.pb.device)
+        mine = torch.empty(n_el, dtype=dt, device=dev)
+        p.copy_intensity(mine.data_ptr())
+        allp = torch.empty((world, n_el), dtype=dt, device=dev)
+        exch.all_gather_into(allp, mine)
+        torch.cuda.synchronize(dev)
+        p.set_intensity([allp[i].data_ptr() for i in range(rank)])
+        return
     if not isinstance(exch, TorchExchange):   # LocalExchange / SimulatedExchange: all ranks in this process
         # the base of rank r reads ranks 0..r-1 before any rank overwrites its
         # own plane, so stage copies first
@@ -174,9 +187,9 @@ def _ospr_plane_exchange(plans, exch, rank_ids, world, cache=None):
         return
     mine = torch.empty(n_el, dtype=dt, device=dev)
     p.copy_intensity(mine.data_ptr())
-    allp = torch.empty((world, n_el), dtype=dt, device=dev)
+    allp = torch.empty(world * n_el, dtype=dt, device=dev)   # flat: what every backend's all-gather accepts
     exch.dist.all_gather_into_tensor(allp, mine, group=exch.group)
-    p.set_intensity([allp[i].data_ptr() for i in range(rank)])
+    p.set_intensity([allp[i * n_el:(i + 1) * n_el].data_ptr() for i in range(rank)])
 
 
 class OsprShardSession:

@@ -241,6 +241,141 @@ class SymmetricExchange(TorchExchange):
         self.handle.barrier(channel=0)
 
 
+class _DevArray:
+    """A raw device allocation seen by torch through __cuda_array_interface__
+    (torch as a view, the library as the allocator: CUDA IPC handles must
+    refer to allocation bases, which torch's caching allocator does not
+    guarantee)."""
+
+    def __init__(self, ptr, shape, typestr):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (int(ptr), False),
+                                         "version": 2, "strides": None}
+
+
+class NcclExchange:
+    """One rank of a distributed run whose data plane is the library's own
+    (cgh_multi_*): the slab buffers are library allocations
+    mapped into every peer with CUDA IPC, the corner turn is the fused
+    peer-store kernel (cgh_slab_turn) followed by the device barrier on peer
+    flags (cgh_multi_device_barrier), and the error sums / gathers are NCCL
+    collectives of the library's communicator on the pass stream. torch.distributed
+    only bootstraps: the broadcast of the NCCL id and the exchange of IPC
+    handles (host objects)."""
+
+    needs_send_buffer = False
+
+    def __init__(self, group=None, device=None, stream=None):
+        import torch
+        import torch.distributed as dist
+
+        self.dist, self.group = dist, group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.device = torch.cuda.current_device() if device is None else int(device)
+        self.lib = _native.library()
+        if not self.lib.cgh_multi_available():
+            raise RuntimeError("NCCL (libnccl.so.2) not available to the library")
+        self.stream = torch.cuda.current_stream(self.device).cuda_stream if stream is None else stream
+        idb = (ctypes.c_uint8 * 128)()
+        if self.rank == 0:
+            _native.check(self.lib.cgh_multi_unique_id(idb))
+        obj = [bytes(idb) if self.rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        idb = (ctypes.c_uint8 * 128).from_buffer_copy(obj[0])
+        self.handle = ctypes.c_void_p()
+        _native.check(self.lib.cgh_multi_create(self.device, self.world, self.rank, idb, ctypes.c_void_p(self.stream),
+                                                ctypes.byref(self.handle)))
+        self._allocs = []
+        # barrier flags of every rank, mapped here
+        flags = ctypes.c_void_p()
+        _native.check(self.lib.cgh_multi_flags(self.handle, ctypes.byref(flags)))
+        ptrs = self._exchange_ptr(flags.value)
+        arr = (ctypes.c_void_p * self.world)(*[ctypes.c_void_p(p) for p in ptrs])
+        _native.check(self.lib.cgh_multi_set_peer_flags(self.handle, arr))
+
+    def _exchange_ptr(self, ptr):
+        """Every rank's device pointer for `ptr`'s allocation, mapped into this
+        process (own entry: `ptr` itself)."""
+        h = (ctypes.c_uint8 * 64)()
+        _native.check(self.lib.cgh_multi_ipc_handle(self.handle, ctypes.c_void_p(ptr), h))
+        got = [None] * self.world
+        self.dist.all_gather_object(got, bytes(h), group=self.group)
+        out = []
+        for g, hb in enumerate(got):
+            if g == self.rank:
+                out.append(ptr)
+                continue
+            p = ctypes.c_void_p()
+            _native.check(self.lib.cgh_multi_ipc_open(self.handle, (ctypes.c_uint8 * 64).from_buffer_copy(hb),
+                                                      ctypes.byref(p)))
+            out.append(p.value)
+        return out
+
+    def alloc(self, ops, shape):
+        import torch
+
+        n = 1
+        for d in shape:
+            n *= int(d)
+        esize = 16 if ops.cdtype == torch.complex128 else 8
+        nbytes = 2 * n * esize
+        ptr = ctypes.c_void_p()
+        _native.check(self.lib.cgh_device_alloc(self.device, nbytes, ctypes.byref(ptr)))
+        self._allocs.append(ptr.value)
+        typestr = "<c16" if esize == 16 else "<c8"
+        buf = torch.as_tensor(_DevArray(ptr.value, (2,) + tuple(shape), typestr), device=f"cuda:{self.device}")
+        self.buf = buf
+        self.half = n * esize                       # byte offset of C inside the allocation
+        self.block_bytes = int(shape[1]) * int(shape[2]) * esize
+        self.peer_base = self._exchange_ptr(ptr.value)
+        return buf[0], buf[1]
+
+    def turn(self, ranks, src, dst):
+        (r,) = ranks
+        off = 0 if dst == "A" else self.half
+        r.ops.turn(getattr(r, src), _fused_turn_targets([b + off for b in self.peer_base], self.rank, self.block_bytes))
+        _native.check(self.lib.cgh_multi_device_barrier(self.handle, ctypes.c_void_p(self.stream)))
+
+    def all_reduce(self, tensors):
+        (t,) = tensors
+        _native.check(self.lib.cgh_multi_all_reduce_sum_f64(self.handle, ctypes.c_void_p(t.data_ptr()), t.numel(),
+                                                             ctypes.c_void_p(self.stream)))
+        return [t]
+
+    def gather(self, tensors):
+        import torch
+
+        (t,) = tensors
+        out = torch.empty((self.world,) + tuple(t.shape), dtype=t.dtype, device=t.device)
+        _native.check(self.lib.cgh_multi_all_gather(self.handle, ctypes.c_void_p(t.data_ptr()),
+                                                    ctypes.c_void_p(out.data_ptr()), t.numel() * t.element_size(),
+                                                    ctypes.c_void_p(self.stream)))
+        return list(out)
+
+    def all_gather_into(self, out, t):
+        """out (world, *t.shape) <- every rank's t (NCCL, pass stream)."""
+        _native.check(self.lib.cgh_multi_all_gather(self.handle, ctypes.c_void_p(t.data_ptr()),
+                                                    ctypes.c_void_p(out.data_ptr()), t.numel() * t.element_size(),
+                                                    ctypes.c_void_p(self.stream)))
+
+    def close(self):
+        import torch
+
+        if self.handle:
+            torch.cuda.synchronize(self.device)
+            self.lib.cgh_multi_destroy(self.handle)
+            self.handle = ctypes.c_void_p()
+        for p in self._allocs:
+            self.lib.cgh_device_free(self.device, ctypes.c_void_p(p))
+        self._allocs = []
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+
 class SimulatedExchange:
     """G virtual ranks in one process on one device (tests): phases run rank
     after rank and no kernel waits on another. With device ops the corner turn

@@ -86,3 +86,77 @@ def test_gloo_world2_sharded_gather(tmp_path):
     # rank 0 ran the first block, rank 1 the second (device index 0 each process)
     assert lines[-1].endswith("ValueError: broken job")
     assert all(ln.split(",")[2] == str(j.cfg["seed"] % 9973) for ln, j in zip(lines[:-1], jobs[:-1]))
+
+
+# ---- OSPR subframe-shard exchange (multi._ospr_plane_exchange) on a real
+# world-size-2 process group: each rank's base = sum of the lower ranks' |R|^2
+# totals. Stand-in plans hold CPU planes; the all-gather is gloo.
+class _PlanStandIn:
+    def __init__(self, rank, shape):
+        import numpy as np
+        import torch
+
+        self.shape = shape
+        self.total = torch.from_numpy(np.full(shape[0] * shape[1], float(rank + 1) * 10.0 + np.arange(shape[0] * shape[1])))
+        self.base = None
+
+        class _Pb:
+            precision = 1     # fp64
+            device = -1       # stand-in: CPU tensors
+        self.pb = _Pb()
+
+    def copy_intensity(self, dst_ptr):
+        import ctypes
+
+        ctypes.memmove(dst_ptr, self.total.data_ptr(), self.total.numel() * 8)
+
+    def set_intensity(self, plane_ptrs):
+        import ctypes
+
+        import numpy as np
+
+        acc = np.zeros(self.total.numel())
+        for p in plane_ptrs:
+            acc += np.ctypeslib.as_array((ctypes.c_double * self.total.numel()).from_address(p))
+        self.base = acc
+
+
+def _ospr_worker(rank, world, port, out_dir):
+    import numpy as np
+    import torch
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2006_10509_b200 import multi
+        from paper_2006_10509_b200.slab import TorchExchange
+
+        plan = _PlanStandIn(rank, (3, 4))
+        orig_empty = torch.empty
+
+        def cpu_empty(*a, **k):   # the exchange allocates on the plan's device; stand-in planes live on the CPU
+            k.pop("device", None)
+            return orig_empty(*a, **k)
+
+        torch.empty = cpu_empty
+        orig_device = torch.device
+        torch.device = lambda *a, **k: orig_device("cpu")
+        try:
+            multi._ospr_plane_exchange([plan], TorchExchange(), [rank], world)
+        finally:
+            torch.empty = orig_empty
+            torch.device = orig_device
+        np.save(os.path.join(out_dir, f"base{rank}.npy"), plan.base)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_ospr_shard_exchange_world2_gloo(tmp_path):
+    import numpy as np
+
+    mp.spawn(_ospr_worker, args=(2, _free_port(), str(tmp_path)), nprocs=2, join=True)
+    n = 12
+    tot = [10.0 * (r + 1) + np.arange(n) for r in range(2)]
+    assert np.array_equal(np.load(tmp_path / "base0.npy"), np.zeros(n))          # rank 0: no lower ranks
+    assert np.array_equal(np.load(tmp_path / "base1.npy"), tot[0])               # rank 1: rank 0's total
