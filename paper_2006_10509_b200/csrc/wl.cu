@@ -185,7 +185,9 @@ int wl_gs_loop(cgh_plan* P, const PassArgs<float>& a, int iters) {
     wl::Args w = wl_args(P, a);
     w.line_sums = static_cast<double*>(S->line_sums.p);
     CGH_TRY(wl_stamp_buf(P, w, 0));
-    const int mode = (P->rescale ? 1 : 0) | (a.gain != 0.0f ? 2 : 0);
+    // MODE bit 2: every pixel inside the metric mask (the projection drops its mask selects)
+    const bool full = P->count_in == double(P->H) * double(P->W);
+    const int mode = (P->rescale ? 1 : 0) | (a.gain != 0.0f ? 2 : 0) | (full ? 4 : 0);
     if (P->profiling) CGH_TRY(prof_mark(P, 16 + 7, true));
     cudaError_t e;
     unsigned* bar = static_cast<unsigned*>(S->bar.p);
@@ -193,7 +195,11 @@ int wl_gs_loop(cgh_plan* P, const PassArgs<float>& a, int iters) {
         case 0: e = wl_loop_m<0>(P, w, iters, bar); break;
         case 1: e = wl_loop_m<1>(P, w, iters, bar); break;
         case 2: e = wl_loop_m<2>(P, w, iters, bar); break;
-        default: e = wl_loop_m<3>(P, w, iters, bar); break;
+        case 3: e = wl_loop_m<3>(P, w, iters, bar); break;
+        case 4: e = wl_loop_m<4>(P, w, iters, bar); break;
+        case 5: e = wl_loop_m<5>(P, w, iters, bar); break;
+        case 6: e = wl_loop_m<6>(P, w, iters, bar); break;
+        default: e = wl_loop_m<7>(P, w, iters, bar); break;
     }
     if (P->profiling) CGH_TRY(prof_mark(P, 16 + 7, false));
     P->launches += 1;

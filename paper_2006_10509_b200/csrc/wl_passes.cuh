@@ -244,11 +244,17 @@ __device__ __forceinline__ void advance_tw(cx<float> (&twA)[15]) {
 template <int PASS, int D>
 __device__ __forceinline__ void stage_a(float2* line_sm, const float2* __restrict__ data, int line, int j0,
                                         cx<float> (&twA)[15], int dbg, int cbeg, int cend) {
+    // chunk c + 1's 16 loads are issued before chunk c is transformed, so the
+    // L2 latency is paid once per stage instead of once per chunk
+    cx<float> nxt[16];
+    load_a<PASS, D>(nxt, data, line, j0 + 32 * cbeg, dbg);
 #pragma unroll 1
     for (int c = cbeg; c < cend; ++c) {
         const int j = j0 + 32 * c;
         cx<float> u[16];
-        load_a<PASS, D>(u, data, line, j, dbg);
+#pragma unroll
+        for (int k = 0; k < 16; ++k) u[k] = nxt[k];
+        if (c + 1 < cend) load_a<PASS, D>(nxt, data, line, j + 32, dbg);
         Dft<16, D, 1, float>::run(u);
 #pragma unroll
         for (int f = 1; f < 16; ++f) u[f] = cmul(u[f], twd<D>(twA[f - 1]));
@@ -335,18 +341,18 @@ struct AddrB {
     }
 };
 
-template <int K = 0>
+template <int OFF = 0, int K = 0>
 __device__ __forceinline__ void ld16_b(cx<float> (&u)[16], const AddrB& ad) {
     if constexpr (K < 16) {
-        u[K] = lds<128 * (K >> 1)>(ad.r[K]);
-        ld16_b<K + 1>(u, ad);
+        u[K] = lds<OFF + 128 * (K >> 1)>(ad.r[K]);
+        ld16_b<OFF, K + 1>(u, ad);
     }
 }
-template <int K = 0>
+template <int OFF = 0, int K = 0>
 __device__ __forceinline__ void st16_b(const cx<float> (&u)[16], const AddrB& ad) {
     if constexpr (K < 16) {
-        sts<128 * (K >> 1)>(ad.r[K], u[K]);
-        st16_b<K + 1>(u, ad);
+        sts<OFF + 128 * (K >> 1)>(ad.r[K], u[K]);
+        st16_b<OFF, K + 1>(u, ad);
     }
 }
 
@@ -359,20 +365,41 @@ __device__ __forceinline__ void twiddle_b(cx<float> (&u)[16], unsigned tb) {
         twiddle_b<D, F + 1>(u, tb);
     }
 }
+// the same twiddles applied to two chunks (one table read each)
+template <int D, int F = 1>
+__device__ __forceinline__ void twiddle_b2(cx<float> (&u)[16], cx<float> (&v)[16], unsigned tb) {
+    if constexpr (F < 16) {
+        const cx<float> w = twd<D>(lds<64 * (F - 1)>(tb));
+        u[F] = cmul(u[F], w);
+        v[F] = cmul(v[F], w);
+        twiddle_b2<D, F + 1>(u, v, tb);
+    }
+}
 
 // FIRST: DIF stage (butterfly, then twiddle); else DIT stage (twiddle, then butterfly)
 template <int D, bool FIRST>
 __device__ __forceinline__ void stage_b_any(float2* line_sm, int lane, unsigned tb, int cbeg, int cend) {
     AddrB ad(line_sm, lane);
     for (int c = 0; c < cbeg; ++c) ad.next();
+    // two chunks per step (their butterflies are independent): twice the
+    // instruction-level parallelism per warp; chunk counts are even
 #pragma unroll 1
-    for (int c = cbeg; c < cend; ++c) {
-        cx<float> u[16];
-        ld16_b(u, ad);
-        if constexpr (FIRST) Dft<16, D, 1, float>::run(u);
-        twiddle_b<D>(u, tb);
-        if constexpr (!FIRST) Dft<16, D, 1, float>::run(u);
-        st16_b(u, ad);
+    for (int c = cbeg; c < cend; c += 2) {
+        cx<float> u[16], v[16];
+        ld16_b<0>(u, ad);
+        ld16_b<4096>(v, ad);
+        if constexpr (FIRST) {
+            Dft<16, D, 1, float>::run(u);
+            Dft<16, D, 1, float>::run(v);
+        }
+        twiddle_b2<D>(u, v, tb);
+        if constexpr (!FIRST) {
+            Dft<16, D, 1, float>::run(u);
+            Dft<16, D, 1, float>::run(v);
+        }
+        st16_b<0>(u, ad);
+        st16_b<4096>(v, ad);
+        ad.next();
         ad.next();
     }
 }
@@ -433,26 +460,52 @@ template <int PASS, int MODE>
 __device__ __forceinline__ void stage_c_chunks(const Args& a, AddrC& ad, const float* tp, int lane, int myline,
                                                float& sdd, float& srr, float& srd, int cbeg, int cend) {
     for (int C = 0; C < cbeg; ++C) ad.next();
+    // the target (beam) values of chunk C + 1 are loaded while chunk C is
+    // transformed (one L2 latency per stage)
+    float4 n0 = make_float4(1.f, 1.f, 1.f, 1.f), n1 = n0;
+    if (tp) {
+        n0 = __ldg(reinterpret_cast<const float4*>(tp + 8 * lane + 256 * cbeg));
+        n1 = __ldg(reinterpret_cast<const float4*>(tp + 8 * lane + 256 * cbeg) + 1);
+    }
 #pragma unroll 1
     for (int C = cbeg; C < cend; ++C) {
         constexpr int D1 = PASS == COL ? -1 : +1;
         constexpr int D2 = -D1;
-        constexpr bool RESCALE = (MODE & 1) != 0, GAIN = (MODE & 2) != 0;
+        constexpr bool RESCALE = (MODE & 1) != 0, GAIN = (MODE & 2) != 0, FULL = (MODE & 4) != 0;
         const int p0 = 8 * lane + 256 * C;
         cx<float> u[8];
         ld8_c(u, ad);
         float tv[8];
-        if (tp) {
-            const float4 t0 = __ldg(reinterpret_cast<const float4*>(tp + p0));
-            const float4 t1 = __ldg(reinterpret_cast<const float4*>(tp + p0) + 1);
-            tv[0] = t0.x; tv[1] = t0.y; tv[2] = t0.z; tv[3] = t0.w;
-            tv[4] = t1.x; tv[5] = t1.y; tv[6] = t1.z; tv[7] = t1.w;
-        } else {
-#pragma unroll
-            for (int e = 0; e < 8; ++e) tv[e] = 1.0f;
+        tv[0] = n0.x; tv[1] = n0.y; tv[2] = n0.z; tv[3] = n0.w;
+        tv[4] = n1.x; tv[5] = n1.y; tv[6] = n1.z; tv[7] = n1.w;
+        if (tp && C + 1 < cend) {
+            n0 = __ldg(reinterpret_cast<const float4*>(tp + p0 + 256));
+            n1 = __ldg(reinterpret_cast<const float4*>(tp + p0 + 256) + 1);
         }
         Dft<8, D1, 1, float>::run(u);
-        if constexpr (PASS == COL) {
+        if constexpr (PASS == COL && FULL) {
+            // every pixel inside the metric mask (MODE bit 2): no mask selects
+            const float gain = a.gain;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                const float x = u[e].x, y = u[e].y;
+                const float r2 = x * x + y * y;
+                const bool pos = r2 > 0.0f;
+                const float ri = pos ? rsqrtf(r2) : 0.0f;
+                const float rr = r2 * ri;
+                const float tt = tv[e];
+                const float d = rr - tt;
+                sdd = fmaf(d, d, sdd);
+                if constexpr (RESCALE) {
+                    srr += r2;
+                    srd = fmaf(rr, d, srd);
+                }
+                float want = tt;
+                if constexpr (GAIN) want = fmaxf(tt + gain * (tt - rr), 0.0f);
+                const float k = want * ri;
+                u[e] = mk(pos ? x * k : want, y * k);
+            }
+        } else if constexpr (PASS == COL) {
             const float gain = a.gain;
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
