@@ -76,6 +76,53 @@ def _default_runner(job, device_index):
         return RUNNERS[job.cfg.algorithm](job.cfg, job.target, job.illumination)
 
 
+def device_runners(devices=(0,)):
+    """Runner table for the reference's own batch driver (controller.run_batch,
+    controller.py:336-356, which calls RUNNERS through controller.execute,
+    controller.py:207-210): every worker thread of its ThreadPoolExecutor is
+    bound to one of ``devices`` on its first call (round robin) and keeps it.
+
+    ``cghkit.algorithms.RUNNERS.update(device_runners(range(n_gpus)))`` turns
+    ``run_batch(jobs, workers=k * n_gpus, ...)`` into a multi-GPU batch while
+    the manifest parsing, per-job derived seeds (controller.py:95-97), error
+    rows (controller.py:328-333) and the manifest-ordered CSV
+    (controller.py:348-355) stay the reference's. Holograms do not depend on the
+    device count: each job's seed is fixed by (base seed, job id)."""
+    import itertools
+    import threading
+
+    from .algorithms import DBS, GS, OSPR, RUNNERS, SA
+    from .runtime import device
+
+    devices = list(devices)
+    if not devices:
+        raise ValueError("need at least one device")
+    counter = itertools.count()
+    lock = threading.Lock()
+    local = threading.local()
+
+    def dev_of_thread():
+        d = getattr(local, "dev", None)
+        if d is None:
+            with lock:
+                d = devices[next(counter) % len(devices)]
+            local.dev = d
+        return d
+
+    def wrap(alg):
+        base = RUNNERS[alg]
+
+        def runner(cfg, target, illumination=None, **kw):
+            with device(dev_of_thread()):
+                return base(cfg, target, illumination, **kw)
+
+        runner.__name__ = base.__name__
+        runner.__doc__ = base.__doc__
+        return runner
+
+    return {alg: wrap(alg) for alg in (GS, SA, DBS, OSPR)}
+
+
 def run_batch(jobs, devices=(0,), runner=None, keep_holograms=True):
     """Run ``jobs`` on ``devices`` (one host thread per device); a failing job
     is recorded and does not abort the batch (controller.py:328-333)."""

@@ -36,3 +36,35 @@ def test_threads_share_the_library_deterministically():
         hb = b.hologram if isinstance(b.hologram, list) else [b.hologram]
         assert all(np.array_equal(x, y) for x, y in zip(ha, hb))
         assert a.report.error_trace == b.report.error_trace
+
+
+def test_device_runners_in_a_reference_style_thread_pool():
+    """multi.device_runners used the way controller.run_batch uses RUNNERS
+    (ThreadPoolExecutor over jobs, controller.py:345-346): per-job outputs equal
+    sequential single-device runs whatever thread ran them."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    import numpy as np
+
+    from paper_2006_10509_b200 import algorithms as A
+    from paper_2006_10509_b200.image import rect_mask
+    from paper_2006_10509_b200.multi import derived_seed, device_runners
+    from paper_2006_10509_b200.propagation import MetricSpec, PropagationSpec
+    from paper_2006_10509_b200.slm import PhaseOnly, SlmSpec
+    from paper_2006_10509_b200.workloads import natural_target
+
+    n = 512
+    target = natural_target(n)
+
+    def cfg_of(job_id):
+        return A.AlgorithmConfig("gs", SlmSpec(n, n, PhaseOnly(8)), PropagationSpec("fresnel"),
+                                 MetricSpec(rect_mask(n, n)), seed=derived_seed(11, job_id), iterations=8)
+
+    ids = [f"job{i}" for i in range(6)]
+    runners = device_runners([0, 0, 0])
+    with ThreadPoolExecutor(max_workers=3) as pool:
+        got = list(pool.map(lambda j: runners["gs"](cfg_of(j), target), ids))
+    for j, (holo, rep) in zip(ids, got):
+        ref_h, ref = A.run_gs(cfg_of(j), target)
+        assert np.array_equal(holo, ref_h)
+        assert rep.error_trace == ref.error_trace
