@@ -6,6 +6,8 @@
 #include <thread>
 
 #include "runtime.cuh"
+#include "host_pool.h"
+#include <cstring>
 
 namespace cgh {
 
@@ -342,10 +344,7 @@ int upload_staged(cgh_plan* P, void* dst, const void* src, size_t bytes) {
             if (cudaEventRecord(P->pin_ev[b], P->pin_st[t]) != cudaSuccess) err = 1;
         }
     };
-    std::vector<std::thread> th;
-    for (int t = 1; t < kStageThreads; ++t) th.emplace_back(worker, t);
-    worker(0);
-    for (auto& x : th) x.join();
+    HostPool::get().run(kStageThreads, worker);
     if (err) return fail(CGH_ERR_CUDA, "staged upload failed");
     for (int t = 0; t < kStageThreads; ++t) {
         CGH_CUDA(cudaEventRecord(P->pin_ev[2 * t], P->pin_st[t]));
@@ -355,6 +354,57 @@ int upload_staged(cgh_plan* P, void* dst, const void* src, size_t bytes) {
     // next call records `start` on P->st, which now waits for them
     return CGH_OK;
 }
+
+#if defined(__SSE2__)
+// One contiguous run of L pixels of the amplitude preparation below, two
+// complex128 values per SSE2 register pair, four pixels per step: out[i] =
+// +-float(|t_i|) (sign bit set outside the mask), streamed; per-run count and
+// sum of |t|^2 inside the mask (fixed order: two lanes, then lane 0 + lane 1).
+// |t| = sqrt(re^2 + im^2) exactly as the scalar path; returns false if a
+// pixel needs the scalar path's care (|t| >= 1e150, a nonzero |t| < 1e-150
+// or squares that underflow to 0, NaN / Inf) or the run is not 4-aligned.
+static bool amp_run_sse2(const double* t, const uint8_t* m, float* o, int L, double& cnt, double& den) {
+    if ((L & 3) || (reinterpret_cast<uintptr_t>(o) & 15u)) return false;
+    const __m128d big = _mm_set1_pd(1e150), small = _mm_set1_pd(1e-150), zd = _mm_setzero_pd();
+    const __m128i zi = _mm_setzero_si128(), sign = _mm_set1_epi32(int(0x80000000u));
+    __m128d dsum = zd;
+    long in_count = 0;
+    int bad = 0;
+    for (int i = 0; i < L; i += 4) {
+        const __m128d x0 = _mm_loadu_pd(t + 2 * i), x1 = _mm_loadu_pd(t + 2 * i + 2);
+        const __m128d x2 = _mm_loadu_pd(t + 2 * i + 4), x3 = _mm_loadu_pd(t + 2 * i + 6);
+        const __m128d s0 = _mm_mul_pd(x0, x0), s1 = _mm_mul_pd(x1, x1);
+        const __m128d s2 = _mm_mul_pd(x2, x2), s3 = _mm_mul_pd(x3, x3);
+        const __m128d a01 = _mm_sqrt_pd(_mm_add_pd(_mm_unpacklo_pd(s0, s1), _mm_unpackhi_pd(s0, s1)));
+        const __m128d a23 = _mm_sqrt_pd(_mm_add_pd(_mm_unpacklo_pd(s2, s3), _mm_unpackhi_pd(s2, s3)));
+        const __m128d q0 = _mm_cmpneq_pd(x0, zd), q1 = _mm_cmpneq_pd(x1, zd);
+        const __m128d q2 = _mm_cmpneq_pd(x2, zd), q3 = _mm_cmpneq_pd(x3, zd);
+        const __m128d nz01 = _mm_or_pd(_mm_unpacklo_pd(q0, q1), _mm_unpackhi_pd(q0, q1));
+        const __m128d nz23 = _mm_or_pd(_mm_unpacklo_pd(q2, q3), _mm_unpackhi_pd(q2, q3));
+        const __m128d f01 = _mm_or_pd(_mm_cmpnlt_pd(a01, big), _mm_and_pd(_mm_cmplt_pd(a01, small), nz01));
+        const __m128d f23 = _mm_or_pd(_mm_cmpnlt_pd(a23, big), _mm_and_pd(_mm_cmplt_pd(a23, small), nz23));
+        bad |= _mm_movemask_pd(_mm_or_pd(f01, f23));
+        uint32_t mb;
+        memcpy(&mb, m + i, 4);
+        // 32-bit lane k all ones where mask byte k is 0 (outside the mask)
+        const __m128i out32 = _mm_cmpeq_epi32(
+            _mm_unpacklo_epi16(_mm_unpacklo_epi8(_mm_cvtsi32_si128(int(mb)), zi), zi), zi);
+        const __m128 af = _mm_movelh_ps(_mm_cvtpd_ps(a01), _mm_cvtpd_ps(a23));
+        _mm_stream_ps(o + i, _mm_xor_ps(af, _mm_castsi128_ps(_mm_and_si128(out32, sign))));
+        const __m128d in01 = _mm_castsi128_pd(_mm_andnot_si128(_mm_unpacklo_epi32(out32, out32), _mm_set1_epi32(-1)));
+        const __m128d in23 = _mm_castsi128_pd(_mm_andnot_si128(_mm_unpackhi_epi32(out32, out32), _mm_set1_epi32(-1)));
+        dsum = _mm_add_pd(dsum, _mm_and_pd(_mm_mul_pd(a01, a01), in01));
+        dsum = _mm_add_pd(dsum, _mm_and_pd(_mm_mul_pd(a23, a23), in23));
+        in_count += 4 - __builtin_popcount(unsigned(_mm_movemask_ps(_mm_castsi128_ps(out32))));
+    }
+    if (bad) return false;
+    double lanes[2];
+    _mm_storeu_pd(lanes, dsum);
+    cnt += double(in_count);
+    den += lanes[0] + lanes[1];
+    return true;
+}
+#endif
 
 // fp32 plans whose runs never start from the backpropagated target: the
 // shifted, mask-signed amplitude plane (prep_kernel's output) and the beam
@@ -416,6 +466,19 @@ static int prep_target_host_f32(cgh_plan* P, const double* target, const uint8_t
             const double* trow = target + 2 * long(uc) * W;
             const uint8_t* mrow = mask + long(uc) * W;
             float* orow = amp + long(u) * W;
+#if defined(__SSE2__)
+            // vectorised row in its two contiguous runs (columns W/2.. then 0..)
+            if (!(W & 1)) {
+                double c = 0, d = 0;
+                const int h = W / 2;
+                if (amp_run_sse2(trow + 2 * long(h), mrow + h, orow, h, c, d) &&
+                    amp_run_sse2(trow, mrow, orow + h, h, c, d)) {
+                    cnt += c;
+                    den += d;
+                    goto beam_row;
+                }
+            }
+#endif
             for (int v = 0; v < W; ++v) {
                 const int vc = v + W / 2 >= W ? v + W / 2 - W : v + W / 2;
                 const double re = trow[2 * vc], im = trow[2 * vc + 1];
@@ -429,18 +492,20 @@ static int prep_target_host_f32(cgh_plan* P, const double* target, const uint8_t
                 }
                 if (!fin) nfa += 1.0;
                 const float af = float(a);
-                orow[v] = in ? af : -af;   // -0.0 for dark pixels outside the mask
+                stream_store_f32(orow + v, in ? af : -af);   // -0.0 for dark pixels outside the mask
             }
+        beam_row:
             if (bamp) {   // the beam is not shifted (hologram plane)
                 const double* irow = illum + 2 * long(u) * W;
                 float* brow = bamp + long(u) * W;
                 for (int v = 0; v < W; ++v) {
                     const double br = irow[2 * v], bi = irow[2 * v + 1];
                     if (!(std::isfinite(br) && std::isfinite(bi))) nfb += 1.0;
-                    brow[v] = float(mag(br, bi));
+                    stream_store_f32(brow + v, float(mag(br, bi)));
                 }
             }
             if (u + 1 - flushed >= rows_per_copy || u + 1 == u1) {
+                stream_fence();   // the streamed rows are in memory before the DMA reads them
                 const size_t off = size_t(flushed) * W, len = size_t(u + 1 - flushed) * W * sizeof(float);
                 if (cudaMemcpyAsync(static_cast<float*>(P->tgt.p) + off, amp + off, len, cudaMemcpyHostToDevice,
                                     P->amp_st[t]) != cudaSuccess)
@@ -458,10 +523,7 @@ static int prep_target_host_f32(cgh_plan* P, const double* target, const uint8_t
         s[3] = nfa;
         s[4] = nfb;
     };
-    std::vector<std::thread> th;
-    for (int t = 1; t < nt; ++t) th.emplace_back(worker, t);
-    worker(0);
-    for (auto& x : th) x.join();
+    HostPool::get().run(nt, worker);
     if (err) return fail(CGH_ERR_CUDA, "amplitude upload failed");
     for (int t = 0; t < nt; ++t) {
         CGH_CUDA(cudaEventRecord(P->amp_ev[t], P->amp_st[t]));
@@ -1424,8 +1486,14 @@ int cgh_expand_states(const void* idx, int32_t idx_bytes, int64_t count, const d
     if (count < 0 || (count > 0 && (!idx || !states || !out)) || (idx_bytes != 1 && idx_bytes != 4))
         return fail(CGH_ERR_VALUE, "bad arguments");
     const int nt = std::max(1, std::min(threads > 0 ? threads : 8, 64));
-    std::vector<std::thread> pool;
     std::atomic<int> bad{0};
+    // streaming 16-byte stores when the output is 16-byte aligned (numpy's
+    // large arrays are): the complex128 plane is written once, never read here
+#if defined(__SSE2__)
+    const bool nt_ok = (reinterpret_cast<uintptr_t>(out) & 15u) == 0;
+#else
+    const bool nt_ok = false;
+#endif
     auto work = [&](int64_t a, int64_t b) {
         for (int64_t i = a; i < b; ++i) {
             const int k = idx_bytes == 1 ? int(static_cast<const uint8_t*>(idx)[i]) : static_cast<const int32_t*>(idx)[i];
@@ -1433,17 +1501,22 @@ int cgh_expand_states(const void* idx, int32_t idx_bytes, int64_t count, const d
                 bad = 1;
                 continue;
             }
+#if defined(__SSE2__)
+            if (nt_ok) {
+                _mm_stream_pd(out + 2 * i, _mm_set_pd(states[2 * k + 1], states[2 * k]));
+                continue;
+            }
+#endif
             out[2 * i] = states[2 * k];
             out[2 * i + 1] = states[2 * k + 1];
         }
+        stream_fence();
     };
     const int64_t chunk = (count + nt - 1) / nt;
-    for (int t = 1; t < nt; ++t) {
+    HostPool::get().run(nt, [&](int t) {
         const int64_t a = t * chunk, b = std::min(count, a + chunk);
-        if (a < b) pool.emplace_back(work, a, b);
-    }
-    work(0, std::min(count, chunk));
-    for (auto& th : pool) th.join();
+        if (a < b) work(a, b);
+    });
     if (bad) return fail(CGH_ERR_VALUE, "index outside the state table");
     return CGH_OK;
 }
@@ -1457,13 +1530,10 @@ int cgh_prefault(void* p, int64_t bytes, int32_t threads) {
         for (int64_t i = a; i < b; ++i) static_cast<volatile char*>(p)[i * kPage] = 0;
     };
     const int64_t chunk = (pages + nt - 1) / nt;
-    std::vector<std::thread> pool;
-    for (int t = 1; t < nt; ++t) {
+    HostPool::get().run(nt, [&](int t) {
         const int64_t a = t * chunk, b = std::min(pages, a + chunk);
-        if (a < b) pool.emplace_back(touch, a, b);
-    }
-    touch(0, std::min(pages, chunk));
-    for (auto& th : pool) th.join();
+        if (a < b) touch(a, b);
+    });
     return CGH_OK;
 }
 

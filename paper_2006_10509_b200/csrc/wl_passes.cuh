@@ -27,9 +27,14 @@
 // Work: a CTA holds 3 quads (4 lines each) and 1 pair (2 lines); per round a
 // grid of G CTAs covers 3G quads plus G pairs (the pairs take half a quad
 // each). At G = 148: 444 + 74 = 518 >= 512 quads, one round.
+//
+// Arithmetic: packed complex64 (pcx.cuh, one f32x2 instruction per complex
+// add / subtract, two per complex product): the passes are issue-bound, and
+// the packed form halves the issue slots of the butterflies and twiddles.
 #pragma once
 #include "fft_block.cuh"
 #include "passes.cuh"
+#include "pcx.cuh"
 
 namespace cgh {
 namespace wl {
@@ -51,9 +56,11 @@ constexpr size_t LINE_BYTES = size_t(N) * 8;
 // bank space, so the joint stages (4 lines x 8 consecutive points per warp
 // instruction) hit every bank pair exactly twice
 constexpr size_t SLOT_BYTES = LINE_BYTES + 32;
-// after the slots: stage-B twiddles w_128^(j' f) as [f - 1][j'] (15 x 8 complex)
+// after the slots: stage-B twiddles w_128^(j' f) as [f - 1][j'] (15 x 8), each
+// stored as {wx, wy, -wy, wy} (the broadcast and the pair of a packed product)
 constexpr size_t TWB_OFF = size_t(LINES) * SLOT_BYTES;
-constexpr size_t SMEM = TWB_OFF + 15 * 8 * 8;
+constexpr size_t TWB_ENTRY = 16;
+constexpr size_t SMEM = TWB_OFF + 15 * 8 * TWB_ENTRY;
 
 enum { ROW = 0, COL = 1 };
 
@@ -126,11 +133,17 @@ __device__ __forceinline__ void stamp(const Args& a, int w, int mark) {
     }
 }
 
-// exp(D * 2 pi i e / N) from the table (D = -1 forward, +1 inverse)
-template <int D>
-__device__ __forceinline__ cx<float> twd(cx<float> w) {
-    if constexpr (D < 0) return w;
-    else return conj(w);
+using pk::pc;
+
+__device__ __forceinline__ unsigned saddr(const void* p) { return unsigned(__cvta_generic_to_shared(p)); }
+
+// global / shared 64-bit accesses of one complex64 value
+__device__ __forceinline__ pc ldcg_pc(const float2* p) {
+    return __ldcg(reinterpret_cast<const unsigned long long*>(p));
+}
+__device__ __forceinline__ void stcg_pc(float2* p, pc v) { __stcg(reinterpret_cast<unsigned long long*>(p), v); }
+__device__ __forceinline__ pc ldg_pc(const cx<float>* p) {
+    return __ldg(reinterpret_cast<const unsigned long long*>(p));
 }
 
 // group geometry of warp `w` (0..15). Quads (groups 0..2): warp wi of the
@@ -196,18 +209,18 @@ __device__ __forceinline__ int round_len() {
 
 // t[f - 1] = tw[(base * f) mod N], f = 1..15 (loaded per stage: only the
 // stage's own twiddles are live)
-__device__ __forceinline__ void load_tw(cx<float> (&t)[15], const cx<float>* __restrict__ tw, int base) {
+__device__ __forceinline__ void load_tw(pc (&t)[15], const cx<float>* __restrict__ tw, int base) {
 #pragma unroll
-    for (int f = 1; f < 16; ++f) t[f - 1] = ldg_cx(tw + ((base * f) & (N - 1)));
+    for (int f = 1; f < 16; ++f) t[f - 1] = ldg_pc(tw + ((base * f) & (N - 1)));
 }
 
 // ---- stage A (joint): load 16 points of butterfly j, radix 16, twiddle, store
 template <int PASS, int D>
-__device__ __forceinline__ void load_a(cx<float> (&u)[16], const float2* __restrict__ data, int line, int j,
+__device__ __forceinline__ void load_a(pc (&u)[16], const float2* __restrict__ data, int line, int j,
                                        int dbg = 0) {
     if (kDebug && (dbg & 2)) {
 #pragma unroll
-        for (int k = 0; k < 16; ++k) u[k] = mk(float(j), float(k));
+        for (int k = 0; k < 16; ++k) u[k] = pk::make(float(j), float(k));
         return;
     }
     const float2* p = data + t4_line<PASS>(line, j);
@@ -222,18 +235,16 @@ __device__ __forceinline__ void load_a(cx<float> (&u)[16], const float2* __restr
         pb[q] = pb[q - 1] + off;
     }
 #pragma unroll
-    for (int k = 0; k < 16; ++k) {
-        const float2 z = __ldcg(PASS == ROW ? pb[k >> 2] + (k & 3) * kStep128<PASS> : p + k * kStep128<PASS>);
-        u[k] = mk(z.x, z.y);
-    }
+    for (int k = 0; k < 16; ++k)
+        u[k] = ldcg_pc(PASS == ROW ? pb[k >> 2] + (k & 3) * kStep128<PASS> : p + k * kStep128<PASS>);
 }
 
 // w_64^f factors that advance the stage-A twiddles from chunk c to c + 1
 // (j -> j + 32: w^(j f) -> w^(j f) w^(32 f)), table (forward) convention
 template <int F = 1>
-__device__ __forceinline__ void advance_tw(cx<float> (&twA)[15]) {
+__device__ __forceinline__ void advance_tw(pc (&twA)[15]) {
     if constexpr (F < 16) {
-        twA[F - 1] = mul_root<float, -1, F, 64>(twA[F - 1]);
+        twA[F - 1] = pk::mul_root<-1, F, 64>(twA[F - 1]);
         advance_tw<F + 1>(twA);
     }
 }
@@ -243,54 +254,51 @@ __device__ __forceinline__ void advance_tw(cx<float> (&twA)[15]) {
 // the line's slot. One code copy for the four chunks (instruction cache).
 template <int PASS, int D>
 __device__ __forceinline__ void stage_a(float2* line_sm, const float2* __restrict__ data, int line, int j0,
-                                        cx<float> (&twA)[15], int dbg, int cbeg, int cend) {
+                                        pc (&twA)[15], int dbg, int cbeg, int cend) {
     // chunk c + 1's 16 loads are issued before chunk c is transformed, so the
     // L2 latency is paid once per stage instead of once per chunk
-    cx<float> nxt[16];
+    pc nxt[16];
     load_a<PASS, D>(nxt, data, line, j0 + 32 * cbeg, dbg);
 #pragma unroll 1
     for (int c = cbeg; c < cend; ++c) {
         const int j = j0 + 32 * c;
-        cx<float> u[16];
+        pc u[16];
 #pragma unroll
         for (int k = 0; k < 16; ++k) u[k] = nxt[k];
         if (c + 1 < cend) load_a<PASS, D>(nxt, data, line, j + 32, dbg);
-        Dft<16, D, 1, float>::run(u);
+        pk::Dft<16, D, 1>::run(u);
 #pragma unroll
-        for (int f = 1; f < 16; ++f) u[f] = cmul(u[f], twd<D>(twA[f - 1]));
+        for (int f = 1; f < 16; ++f) u[f] = pk::cmul_d<D>(u[f], twA[f - 1]);
         const SwzA sa(j);
+        pc* lp = reinterpret_cast<pc*>(line_sm);
 #pragma unroll
-        for (int f = 0; f < 16; ++f) line_sm[sa(f)] = make_float2(u[f].x, u[f].y);
+        for (int f = 0; f < 16; ++f) lp[sa(f)] = u[f];
         if (c + 1 < cend) advance_tw(twA);
     }
 }
-
-__device__ __forceinline__ int k_dummy_line(int line) { return line; }
 
 // ---- stage A' (joint): load the 16 spectrum blocks of butterfly j, twiddle,
 // radix 16, store to HBM/L2
 template <int PASS, int D>
 __device__ __forceinline__ void stage_a2(const float2* line_sm, float2* __restrict__ data, int line, int j0,
-                                         cx<float> (&twA)[15], int dbg, int cbeg, int cend) {
+                                         pc (&twA)[15], int dbg, int cbeg, int cend) {
 #pragma unroll 1
     for (int c = cbeg; c < cend; ++c) {
         const int j = j0 + 32 * c;
-        cx<float> u[16];
+        pc u[16];
         const SwzA sa(j);
+        const pc* lp = reinterpret_cast<const pc*>(line_sm);
 #pragma unroll
-        for (int f = 0; f < 16; ++f) {
-            const float2 z = line_sm[sa(f)];
-            u[f] = mk(z.x, z.y);
-        }
+        for (int f = 0; f < 16; ++f) u[f] = lp[sa(f)];
 #pragma unroll
-        for (int f = 1; f < 16; ++f) u[f] = cmul(u[f], twd<D>(twA[f - 1]));
-        Dft<16, D, 1, float>::run(u);
+        for (int f = 1; f < 16; ++f) u[f] = pk::cmul_d<D>(u[f], twA[f - 1]);
+        pk::Dft<16, D, 1>::run(u);
         if (c + 1 < cend) advance_tw(twA);
         float2* p = data + t4_line<PASS>(line, j);
         if (kDebug && (dbg & 2)) {   // timing: arithmetic kept, no stores
 #pragma unroll
             for (int k = 0; k < 16; ++k)
-                if (u[k].x == 1234.5f) __stcg(p, make_float2(u[k].x, u[k].y));
+                if (pk::re(u[k]) == 1234.5f) stcg_pc(p, u[k]);
             continue;
         }
         float2* pb[4];
@@ -303,22 +311,27 @@ __device__ __forceinline__ void stage_a2(const float2* line_sm, float2* __restri
         }
 #pragma unroll
         for (int k = 0; k < 16; ++k)
-            __stcg(PASS == ROW ? pb[k >> 2] + (k & 3) * kStep128<PASS> : p + k * kStep128<PASS>,
-                   make_float2(u[k].x, u[k].y));
+            stcg_pc(PASS == ROW ? pb[k >> 2] + (k & 3) * kStep128<PASS> : p + k * kStep128<PASS>, u[k]);
     }
 }
 
 // ---- shared-memory access with precomputed swizzled addresses
-__device__ __forceinline__ unsigned saddr(const void* p) { return unsigned(__cvta_generic_to_shared(p)); }
 template <int OFF>
-__device__ __forceinline__ cx<float> lds(unsigned a) {
-    float x, y;
-    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2+%3];" : "=f"(x), "=f"(y) : "r"(a), "n"(OFF));
-    return mk(x, y);
+__device__ __forceinline__ pc lds(unsigned a) {
+    pc v;
+    asm volatile("ld.shared.b64 %0, [%1+%2];" : "=l"(v) : "r"(a), "n"(OFF));
+    return v;
 }
 template <int OFF>
-__device__ __forceinline__ void sts(unsigned a, cx<float> v) {
-    asm volatile("st.shared.v2.f32 [%0+%1], {%2, %3};" ::"r"(a), "n"(OFF), "f"(v.x), "f"(v.y) : "memory");
+__device__ __forceinline__ void sts(unsigned a, pc v) {
+    asm volatile("st.shared.b64 [%0+%1], %2;" ::"r"(a), "n"(OFF), "l"(v) : "memory");
+}
+// stage-B twiddle entry {wx, wy, -wy, wy}: the broadcast wx and the pair wn
+template <int OFF>
+__device__ __forceinline__ void lds_tw(unsigned a, float& wx, pc& wn) {
+    pc w0;
+    asm volatile("ld.shared.v2.b64 {%0, %1}, [%2+%3];" : "=l"(w0), "=l"(wn) : "r"(a), "n"(OFF));
+    wx = pk::re(w0);
 }
 
 // ---- stage B / B' (own line): radix 16 on stride 8 inside each 128-block.
@@ -342,14 +355,14 @@ struct AddrB {
 };
 
 template <int OFF = 0, int K = 0>
-__device__ __forceinline__ void ld16_b(cx<float> (&u)[16], const AddrB& ad) {
+__device__ __forceinline__ void ld16_b(pc (&u)[16], const AddrB& ad) {
     if constexpr (K < 16) {
         u[K] = lds<OFF + 128 * (K >> 1)>(ad.r[K]);
         ld16_b<OFF, K + 1>(u, ad);
     }
 }
 template <int OFF = 0, int K = 0>
-__device__ __forceinline__ void st16_b(const cx<float> (&u)[16], const AddrB& ad) {
+__device__ __forceinline__ void st16_b(const pc (&u)[16], const AddrB& ad) {
     if constexpr (K < 16) {
         sts<OFF + 128 * (K >> 1)>(ad.r[K], u[K]);
         st16_b<OFF, K + 1>(u, ad);
@@ -357,21 +370,15 @@ __device__ __forceinline__ void st16_b(const cx<float> (&u)[16], const AddrB& ad
 }
 
 // twiddles of stage B from the shared table (lane j' reads row f: 8 distinct
-// words per instruction, one wavefront)
+// entries per instruction), applied to two chunks (one table read each)
 template <int D, int F = 1>
-__device__ __forceinline__ void twiddle_b(cx<float> (&u)[16], unsigned tb) {
+__device__ __forceinline__ void twiddle_b2(pc (&u)[16], pc (&v)[16], unsigned tb) {
     if constexpr (F < 16) {
-        u[F] = cmul(u[F], twd<D>(lds<64 * (F - 1)>(tb)));
-        twiddle_b<D, F + 1>(u, tb);
-    }
-}
-// the same twiddles applied to two chunks (one table read each)
-template <int D, int F = 1>
-__device__ __forceinline__ void twiddle_b2(cx<float> (&u)[16], cx<float> (&v)[16], unsigned tb) {
-    if constexpr (F < 16) {
-        const cx<float> w = twd<D>(lds<64 * (F - 1)>(tb));
-        u[F] = cmul(u[F], w);
-        v[F] = cmul(v[F], w);
+        float wx;
+        pc wn;
+        lds_tw<8 * int(TWB_ENTRY) * (F - 1)>(tb, wx, wn);
+        u[F] = pk::cmul_d<D>(u[F], wx, wn);
+        v[F] = pk::cmul_d<D>(v[F], wx, wn);
         twiddle_b2<D, F + 1>(u, v, tb);
     }
 }
@@ -385,17 +392,17 @@ __device__ __forceinline__ void stage_b_any(float2* line_sm, int lane, unsigned 
     // instruction-level parallelism per warp; chunk counts are even
 #pragma unroll 1
     for (int c = cbeg; c < cend; c += 2) {
-        cx<float> u[16], v[16];
+        pc u[16], v[16];
         ld16_b<0>(u, ad);
         ld16_b<4096>(v, ad);
         if constexpr (FIRST) {
-            Dft<16, D, 1, float>::run(u);
-            Dft<16, D, 1, float>::run(v);
+            pk::Dft<16, D, 1>::run(u);
+            pk::Dft<16, D, 1>::run(v);
         }
         twiddle_b2<D>(u, v, tb);
         if constexpr (!FIRST) {
-            Dft<16, D, 1, float>::run(u);
-            Dft<16, D, 1, float>::run(v);
+            pk::Dft<16, D, 1>::run(u);
+            pk::Dft<16, D, 1>::run(v);
         }
         st16_b<0>(u, ad);
         st16_b<4096>(v, ad);
@@ -404,7 +411,7 @@ __device__ __forceinline__ void stage_b_any(float2* line_sm, int lane, unsigned 
     }
 }
 __device__ __forceinline__ unsigned twb_addr(const float2* wsm, int lane) {
-    return saddr(reinterpret_cast<const char*>(wsm) + TWB_OFF) + 8u * unsigned(lane & 7);
+    return saddr(reinterpret_cast<const char*>(wsm) + TWB_OFF) + unsigned(TWB_ENTRY) * unsigned(lane & 7);
 }
 template <int D>
 __device__ __forceinline__ void stage_b(float2* line_sm, int lane, unsigned tb, int cbeg, int cend) {
@@ -416,11 +423,11 @@ __device__ __forceinline__ void stage_b2(float2* line_sm, int lane, unsigned tb,
 }
 // fill the stage-B table (whole CTA, before the first pass)
 __device__ __forceinline__ void init_twb(float2* wsm, const cx<float>* __restrict__ tw) {
-    float2* t = reinterpret_cast<float2*>(reinterpret_cast<char*>(wsm) + TWB_OFF);
+    float4* t = reinterpret_cast<float4*>(reinterpret_cast<char*>(wsm) + TWB_OFF);
     for (int i = threadIdx.x; i < 120; i += blockDim.x) {
         const int f = i / 8 + 1, jp = i % 8;
         const cx<float> z = ldg_cx(tw + ((16 * jp * f) & (N - 1)));
-        t[i] = make_float2(z.x, z.y);
+        t[i] = make_float4(z.x, z.y, -z.y, z.y);
     }
 }
 
@@ -440,115 +447,146 @@ struct AddrC {
         for (int e = 0; e < 8; ++e) r[e] += 2048u;
     }
 };
-template <int E = 0>
-__device__ __forceinline__ void ld8_c(cx<float> (&u)[8], const AddrC& ad) {
+template <int OFF = 0, int E = 0>
+__device__ __forceinline__ void ld8_c(pc (&u)[8], const AddrC& ad) {
     if constexpr (E < 8) {
-        u[E] = lds<0>(ad.r[E]);
-        ld8_c<E + 1>(u, ad);
+        u[E] = lds<OFF>(ad.r[E]);
+        ld8_c<OFF, E + 1>(u, ad);
     }
 }
-template <int E = 0>
-__device__ __forceinline__ void st8_c(const cx<float> (&u)[8], const AddrC& ad) {
+template <int OFF = 0, int E = 0>
+__device__ __forceinline__ void st8_c(const pc (&u)[8], const AddrC& ad) {
     if constexpr (E < 8) {
-        sts<0>(ad.r[E], u[E]);
-        st8_c<E + 1>(u, ad);
+        sts<OFF>(ad.r[E], u[E]);
+        st8_c<OFF, E + 1>(u, ad);
     }
 }
 
-// ---- stage C (own line): radix 8, projection, radix 8 (second transform)
+// ---- stage C pointwise step on the 8 spectrum points of one chunk (digit-
+// reversed positions p0 .. p0 + 7, target / beam values tv)
+template <int PASS, int MODE>
+__device__ __forceinline__ void project8(const Args& a, pc (&u)[8], const float (&tv)[8], const float* tp, int p0,
+                                         int myline, float& sdd, float& srr, float& srd) {
+    constexpr bool RESCALE = (MODE & 1) != 0, GAIN = (MODE & 2) != 0, FULL = (MODE & 4) != 0;
+    if constexpr (PASS == COL && FULL) {
+        // every pixel inside the metric mask (MODE bit 2): no mask selects
+        const float gain = a.gain;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const float x = pk::re(u[e]), y = pk::im(u[e]);
+            const float r2 = x * x + y * y;
+            const bool pos = r2 > 0.0f;
+            const float ri = pos ? rsqrtf(r2) : 0.0f;
+            const float rr = r2 * ri;
+            const float tt = tv[e];
+            const float d = rr - tt;
+            sdd = fmaf(d, d, sdd);
+            if constexpr (RESCALE) {
+                srr += r2;
+                srd = fmaf(rr, d, srd);
+            }
+            float want = tt;
+            if constexpr (GAIN) want = fmaxf(tt + gain * (tt - rr), 0.0f);
+            const float k = want * ri;
+            const pc sc = pk::mul(u[e], pk::bc(k));
+            u[e] = pos ? sc : pk::make(want, pk::im(sc));
+        }
+    } else if constexpr (PASS == COL) {
+        const float gain = a.gain;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const float x = pk::re(u[e]), y = pk::im(u[e]);
+            const float r2 = x * x + y * y;
+            const float ri = rsqrtf(r2);   // inf at 0
+            const float rr = r2 > 0.0f ? r2 * ri : 0.0f;
+            const float tt = tv[e];
+            const bool in = !signbit(tt);
+            const float d = rr - tt;
+            sdd += in ? d * d : 0.0f;
+            if constexpr (RESCALE) {
+                srr += in ? r2 : 0.0f;
+                srd += in ? rr * d : 0.0f;
+            }
+            float want = tt;
+            if constexpr (GAIN) want = fmaxf(tt + gain * (tt - rr), 0.0f);
+            const bool pos = r2 > 0.0f;
+            const float k = in ? (pos ? want * ri : 0.0f) : 1.0f;
+            u[e] = pk::make(x * k + ((in && !pos) ? want : 0.0f), y * k);
+        }
+    } else {
+        unsigned zero = 0;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const float amp = tv[e];
+            const float x = pk::re(u[e]), y = pk::im(u[e]);
+            const float m2 = x * x + y * y;
+            const float k = amp * rsqrtf(m2);
+            if (m2 > 0.0f) u[e] = pk::mul(u[e], pk::bc(k));
+            else zero |= 1u << e;
+        }
+        if (zero) {   // exact zeros: arg 0 -> beam (* q for Fresnel), as fast_row_holo
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+                if ((zero >> e) & 1u) {
+                    cx<float> h = mk(tp ? tp[p0 + e] : 1.0f, 0.0f);
+                    if (a.q_row) h = cmul(h, cmul(a.q_row[myline], a.q_col[natural(p0 + e)]));
+                    u[e] = pk::from(h);
+                }
+        }
+    }
+}
+
+__device__ __forceinline__ void unpack8(float (&t)[8], float4 lo, float4 hi) {
+    t[0] = lo.x; t[1] = lo.y; t[2] = lo.z; t[3] = lo.w;
+    t[4] = hi.x; t[5] = hi.y; t[6] = hi.z; t[7] = hi.w;
+}
+
+// ---- stage C (own line): radix 8, projection, radix 8 (second transform),
+// two chunks per step (independent: twice the instruction-level parallelism
+// per warp; chunk counts are even)
 template <int PASS, int MODE>
 __device__ __forceinline__ void stage_c_chunks(const Args& a, AddrC& ad, const float* tp, int lane, int myline,
                                                float& sdd, float& srr, float& srd, int cbeg, int cend) {
+    constexpr int D1 = PASS == COL ? -1 : +1;
+    constexpr int D2 = -D1;
     for (int C = 0; C < cbeg; ++C) ad.next();
-    // the target (beam) values of chunk C + 1 are loaded while chunk C is
-    // transformed (one L2 latency per stage)
-    float4 n0 = make_float4(1.f, 1.f, 1.f, 1.f), n1 = n0;
+    // the target (beam) values of the next chunk pair are loaded while this
+    // pair is transformed (one L2 latency per stage)
+    float4 n[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) n[q] = make_float4(1.f, 1.f, 1.f, 1.f);
     if (tp) {
-        n0 = __ldg(reinterpret_cast<const float4*>(tp + 8 * lane + 256 * cbeg));
-        n1 = __ldg(reinterpret_cast<const float4*>(tp + 8 * lane + 256 * cbeg) + 1);
+        const float4* t4p = reinterpret_cast<const float4*>(tp + 8 * lane + 256 * cbeg);
+        n[0] = __ldg(t4p);
+        n[1] = __ldg(t4p + 1);
+        n[2] = __ldg(t4p + 64);
+        n[3] = __ldg(t4p + 65);
     }
 #pragma unroll 1
-    for (int C = cbeg; C < cend; ++C) {
-        constexpr int D1 = PASS == COL ? -1 : +1;
-        constexpr int D2 = -D1;
-        constexpr bool RESCALE = (MODE & 1) != 0, GAIN = (MODE & 2) != 0, FULL = (MODE & 4) != 0;
+    for (int C = cbeg; C < cend; C += 2) {
         const int p0 = 8 * lane + 256 * C;
-        cx<float> u[8];
-        ld8_c(u, ad);
-        float tv[8];
-        tv[0] = n0.x; tv[1] = n0.y; tv[2] = n0.z; tv[3] = n0.w;
-        tv[4] = n1.x; tv[5] = n1.y; tv[6] = n1.z; tv[7] = n1.w;
-        if (tp && C + 1 < cend) {
-            n0 = __ldg(reinterpret_cast<const float4*>(tp + p0 + 256));
-            n1 = __ldg(reinterpret_cast<const float4*>(tp + p0 + 256) + 1);
+        pc u[8], v[8];
+        ld8_c<0>(u, ad);
+        ld8_c<2048>(v, ad);
+        float tu[8], tw[8];
+        unpack8(tu, n[0], n[1]);
+        unpack8(tw, n[2], n[3]);
+        if (tp && C + 2 < cend) {
+            const float4* t4p = reinterpret_cast<const float4*>(tp + p0 + 512);
+            n[0] = __ldg(t4p);
+            n[1] = __ldg(t4p + 1);
+            n[2] = __ldg(t4p + 64);
+            n[3] = __ldg(t4p + 65);
         }
-        Dft<8, D1, 1, float>::run(u);
-        if constexpr (PASS == COL && FULL) {
-            // every pixel inside the metric mask (MODE bit 2): no mask selects
-            const float gain = a.gain;
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-                const float x = u[e].x, y = u[e].y;
-                const float r2 = x * x + y * y;
-                const bool pos = r2 > 0.0f;
-                const float ri = pos ? rsqrtf(r2) : 0.0f;
-                const float rr = r2 * ri;
-                const float tt = tv[e];
-                const float d = rr - tt;
-                sdd = fmaf(d, d, sdd);
-                if constexpr (RESCALE) {
-                    srr += r2;
-                    srd = fmaf(rr, d, srd);
-                }
-                float want = tt;
-                if constexpr (GAIN) want = fmaxf(tt + gain * (tt - rr), 0.0f);
-                const float k = want * ri;
-                u[e] = mk(pos ? x * k : want, y * k);
-            }
-        } else if constexpr (PASS == COL) {
-            const float gain = a.gain;
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-                const float x = u[e].x, y = u[e].y;
-                const float r2 = x * x + y * y;
-                const float ri = rsqrtf(r2);   // inf at 0
-                const float rr = r2 > 0.0f ? r2 * ri : 0.0f;
-                const float tt = tv[e];
-                const bool in = !signbit(tt);
-                const float d = rr - tt;
-                sdd += in ? d * d : 0.0f;
-                if constexpr (RESCALE) {
-                    srr += in ? r2 : 0.0f;
-                    srd += in ? rr * d : 0.0f;
-                }
-                float want = tt;
-                if constexpr (GAIN) want = fmaxf(tt + gain * (tt - rr), 0.0f);
-                const bool pos = r2 > 0.0f;
-                const float k = in ? (pos ? want * ri : 0.0f) : 1.0f;
-                u[e] = mk(x * k + ((in && !pos) ? want : 0.0f), y * k);
-            }
-        } else {
-            unsigned zero = 0;
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-                const float amp = tv[e];
-                const float m2 = u[e].x * u[e].x + u[e].y * u[e].y;
-                const float k = amp * rsqrtf(m2);
-                if (m2 > 0.0f) u[e] = mk(u[e].x * k, u[e].y * k);
-                else zero |= 1u << e;
-            }
-            if (zero) {   // exact zeros: arg 0 -> beam (* q for Fresnel), as fast_row_holo
-#pragma unroll
-                for (int e = 0; e < 8; ++e)
-                    if ((zero >> e) & 1u) {
-                        cx<float> h = mk(tp ? tp[p0 + e] : 1.0f, 0.0f);
-                        if (a.q_row) h = cmul(h, cmul(a.q_row[myline], a.q_col[natural(p0 + e)]));
-                        u[e] = h;
-                    }
-            }
-        }
-        Dft<8, D2, 1, float>::run(u);
-        st8_c(u, ad);
+        pk::Dft<8, D1, 1>::run(u);
+        pk::Dft<8, D1, 1>::run(v);
+        project8<PASS, MODE>(a, u, tu, tp, p0, myline, sdd, srr, srd);
+        project8<PASS, MODE>(a, v, tw, tp, p0 + 256, myline, sdd, srr, srd);
+        pk::Dft<8, D2, 1>::run(u);
+        pk::Dft<8, D2, 1>::run(v);
+        st8_c<0>(u, ad);
+        st8_c<2048>(v, ad);
+        ad.next();
         ad.next();
     }
 }
@@ -586,7 +624,7 @@ __device__ __forceinline__ void pass_body(const Args& a, float2* wsm, double* li
 
         if (h2 && !a.no_stagger) asm volatile("bar.sync 5, %0;" ::"r"(THREADS) : "memory");
         if (line0 >= 0) {
-            cx<float> twA[15];
+            pc twA[15];
             load_tw(twA, a.tw, ro.j0 + 32 * a0);
             stage_a<PASS, D1>(gsm, a.data, line, ro.j0, twA, a.debug, a0, a1);
         }
@@ -638,7 +676,7 @@ __device__ __forceinline__ void pass_body(const Args& a, float2* wsm, double* li
             }
         }
         {
-            cx<float> twA[15];
+            pc twA[15];
             load_tw(twA, a.tw, ro.j0 + 32 * a0);
             stage_a2<PASS, D2>(gsm, a.data, line, ro.j0, twA, a.debug, a0, a1);
         }
