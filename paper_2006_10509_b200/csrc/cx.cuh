@@ -1,6 +1,7 @@
 // Complex arithmetic and compile-time roots of unity for the FFT passes.
 #pragma once
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 namespace cgh {
@@ -34,6 +35,56 @@ __device__ __forceinline__ cx<T> cmulc(cx<T> a, cx<T> b) {
 }
 template <class T>
 __device__ __forceinline__ cx<T> conj(cx<T> a) { return mk(a.x, -a.y); }
+
+// ---- complex64 in packed f32x2 instructions (sm_100a FADD2 / FMUL2 /
+// FFMA2): the value's two halves are one 64-bit register pair; a complex add
+// is one instruction instead of two and a complex product two instead of
+// four (see pcx.cuh). Same IEEE roundings per component as the scalar forms.
+// Non-template overloads: preferred to the templates above for cx<float>.
+namespace f2 {
+__device__ __forceinline__ unsigned long long pack(cx<float> a) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a.x), "f"(a.y));
+    return r;
+}
+__device__ __forceinline__ cx<float> unpack(unsigned long long r) {
+    cx<float> a;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a.x), "=f"(a.y) : "l"(r));
+    return a;
+}
+__device__ __forceinline__ unsigned long long mul(unsigned long long a, unsigned long long b) {
+    unsigned long long r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ unsigned long long fma(unsigned long long a, unsigned long long b, unsigned long long c) {
+    unsigned long long r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+}  // namespace f2
+
+__device__ __forceinline__ cx<float> operator+(cx<float> a, cx<float> b) {
+    unsigned long long r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2::pack(a)), "l"(f2::pack(b)));
+    return f2::unpack(r);
+}
+__device__ __forceinline__ cx<float> operator-(cx<float> a, cx<float> b) {
+    unsigned long long r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2::pack(a)), "l"(f2::pack(b)));
+    return f2::unpack(r);
+}
+__device__ __forceinline__ cx<float> operator*(cx<float> a, float s) {
+    return f2::unpack(f2::mul(f2::pack(a), f2::pack(mk(s, s))));
+}
+// a * b = b.x * a + b.y * (-a.y, a.x)
+__device__ __forceinline__ cx<float> cmul(cx<float> a, cx<float> b) {
+    return f2::unpack(f2::fma(f2::pack(mk(a.y, a.x)), f2::pack(mk(-b.y, b.y)), f2::mul(f2::pack(a), f2::pack(mk(b.x, b.x)))));
+}
+// a * conj(b) = b.x * a + b.y * (a.y, -a.x)
+__device__ __forceinline__ cx<float> cmulc(cx<float> a, cx<float> b) {
+    return f2::unpack(f2::fma(f2::pack(mk(a.y, a.x)), f2::pack(mk(b.y, -b.y)), f2::mul(f2::pack(a), f2::pack(mk(b.x, b.x)))));
+}
 
 // Read-only cached load of a complex value.
 __device__ __forceinline__ cx<float> ldg_cx(const cx<float>* p) {
@@ -137,6 +188,12 @@ __device__ __forceinline__ cx<T> mul_root(cx<T> a) {
         return mk(-a.x, -a.y);
     } else if constexpr (4 * m == 3 * R) {
         return rot90<-DIR>(a);
+    } else if constexpr (std::is_same<T, float>::value) {
+        // compile-time root c + i s: c * a + s * (-a.y, a.x), the constants as
+        // immediate / uniform operands of one FMUL2 and one FFMA2
+        constexpr float c = float(detail::rcos(m, R));
+        constexpr float s = float(DIR * detail::rsin(m, R));
+        return f2::unpack(f2::fma(f2::pack(mk(a.y, a.x)), f2::pack(mk(-s, s)), f2::mul(f2::pack(a), f2::pack(mk(c, c)))));
     } else {
         return cmul(a, twc<T, DIR, m, R>());
     }

@@ -49,6 +49,23 @@ struct Dft<4, DIR, S, T> {
     }
 };
 
+// complex64: b +- DIR i d as one FFMA2 each (the swap and the signs are
+// operand modifiers), the other butterflies as FADD2
+template <int DIR, int S>
+struct Dft<4, DIR, S, float> {
+    __device__ __forceinline__ static void run(cx<float>* v) {
+        const cx<float> a = v[0] + v[2 * S], b = v[0] - v[2 * S];
+        const cx<float> c = v[S] + v[3 * S], d = v[S] - v[3 * S];
+        v[0] = a + c;
+        v[2 * S] = a - c;
+        // DIR < 0: b + (d.y, -d.x) ; DIR > 0: b + (-d.y, d.x)
+        const float sp = DIR < 0 ? 1.0f : -1.0f;
+        const unsigned long long ds = f2::pack(mk(d.y, d.x)), bb = f2::pack(b);
+        v[S] = f2::unpack(f2::fma(ds, f2::pack(mk(sp, -sp)), bb));
+        v[3 * S] = f2::unpack(f2::fma(ds, f2::pack(mk(-sp, sp)), bb));
+    }
+};
+
 // R = R1 * R2 split ("four-step in registers"): n = R2*n1 + n2, k = k1 + R1*k2.
 template <int R1, int R2, int DIR, int S, class T>
 struct DftSplit {
