@@ -846,7 +846,9 @@ static int ospr_exec(cgh_plan* P, const cgh_ospr_params* op, int64_t* tk, double
     if (P->count_in == 0) return fail(CGH_ERR_EMPTY_MASK, "metric mask has no true pixels");
     if (P->denom == 0) return fail(CGH_ERR_ZERO_TARGET, "target is zero inside the mask");
     const bool has_cancel = cb && cb->cancel, has_progress = cb && cb->progress;
-    const int G = (has_cancel || has_progress) ? 1 : std::min(S, 64);
+    int gmax = 64;
+    if (const char* e = getenv("CGHB200_OSPR_GROUP")) gmax = std::max(1, std::min(64, atoi(e)));
+    const int G = (has_cancel || has_progress) ? 1 : std::min(S, gmax);
     const long n = long(P->H) * P->W;
     CGH_TRY(ensure(P, P->data, size_t(n) * sizeof(cx<T>) * std::max(G, 1)));
     CGH_TRY(ensure(P, P->idx, size_t(n) * P->idx_bytes * std::max(S, 1)));
