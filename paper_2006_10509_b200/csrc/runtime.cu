@@ -873,7 +873,16 @@ static int ospr_exec(cgh_plan* P, const cgh_ospr_params* op, int64_t* tk, double
     pq.kbias = 1;   // progress(len(frames), err)
     int done = 0;
     bool stop = false;
-    for (int g0 = 0; g0 < S; g0 += G) {
+    int g_start = 0;
+    if constexpr (sizeof(T) == 4) {
+        // 2048^2 fp32 without hooks: every subframe in one persistent launch
+        if (S > 0 && !has_cancel && !has_progress && wl_ospr_eligible(P) && P->idx_bytes == 1) {
+            CGH_TRY(wl_ospr_run(P, a, S));
+            done = S;
+            g_start = S;
+        }
+    }
+    for (int g0 = g_start; g0 < S; g0 += G) {
         if (cancelled(cb)) {
             stop = true;
             break;

@@ -136,6 +136,8 @@ int wl_relayout(cgh_plan* P, int to_t4);
 int wl_col(cgh_plan* P, const PassArgs<float>& a);
 int wl_row(cgh_plan* P, const PassArgs<float>& a);
 int wl_gs_loop(cgh_plan* P, const PassArgs<float>& a, int iters);
+bool wl_ospr_eligible(cgh_plan* P);
+int wl_ospr_run(cgh_plan* P, const PassArgs<float>& a, int S_frames);
 void wl_free(cgh_plan* P);
 void wl_invalidate_target(cgh_plan* P);
 bool fast_ospr_eligible(cgh_plan* P);

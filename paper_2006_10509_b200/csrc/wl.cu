@@ -2,6 +2,7 @@
 #include "launch.cuh"
 #include "runtime.cuh"
 #include "wl_passes.cuh"
+#include "wl_ospr.cuh"
 
 namespace cgh {
 
@@ -10,6 +11,11 @@ struct WlState {
     const void* tgt_src = nullptr;
     const void* beam_src = nullptr;
     bool beam_ready = false;
+    // OSPR: row-ordered target table, column-ordered beam table, line states,
+    // intensity, digit-reversed index bytes, per-row sums
+    DevBuf o_tgt, o_beam, o_states, o_inten, o_idx, o_sums, o_jumps;
+    const void* o_tgt_src = nullptr;
+    bool o_beam_ready = false;
 };
 
 static WlState* wl_state(cgh_plan* P) { return static_cast<WlState*>(P->wlst); }
@@ -23,7 +29,9 @@ bool wl_eligible(cgh_plan* P) {
 void wl_free(cgh_plan* P) {
     WlState* S = wl_state(P);
     if (!S) return;
-    DevBuf* bufs[] = {&S->t4, &S->tgt_perm, &S->beam_perm, &S->line_sums, &S->stamps, &S->bar};
+    DevBuf* bufs[] = {&S->t4,      &S->tgt_perm, &S->beam_perm, &S->line_sums, &S->stamps, &S->bar,
+                      &S->o_tgt,   &S->o_beam,   &S->o_states,  &S->o_inten,   &S->o_idx,   &S->o_sums,
+                      &S->o_jumps};
     for (DevBuf* b : bufs)
         if (b->p) cudaFreeAsync(b->p, P->st);
     delete S;
@@ -35,6 +43,8 @@ void wl_invalidate_target(cgh_plan* P) {
     if (S) {
         S->tgt_src = nullptr;
         S->beam_ready = false;
+        S->o_tgt_src = nullptr;
+        S->o_beam_ready = false;
     }
 }
 
@@ -207,6 +217,123 @@ int wl_gs_loop(cgh_plan* P, const PassArgs<float>& a, int iters) {
     wl::wl_trace_kernel<<<std::min(iters, 148), 96, 0, P->st>>>(w.line_sums, iters, a.red.denom, P->rescale ? 1 : 0,
                                                                P->res_d);
     P->launches += 1;
+    CGH_CUDA(cudaGetLastError());
+    return CGH_OK;
+}
+
+// Opt-in (CGHB200_WL_OSPR=1): measured on B200 at 2048^2 x 24 binary, the
+// loop takes 1.54 ms + 0.25 ms of table / permute kernels against 1.62 ms for
+// the batched fast passes (fast_ospr_gen / fast_col_holo / fast_ospr_acc):
+// OSPR's per-pixel PCG64 draws and snapping, not its plane traffic, bound both
+// (DESIGN.md section 3.2), so the default stays with the batched passes.
+bool wl_ospr_eligible(cgh_plan* P) {
+    return wl_eligible(P) && getenv("CGHB200_WL_OSPR") != nullptr;
+}
+
+// All S subframes of run_ospr in one persistent launch (wl_ospr.cuh), then
+// the per-subframe errors / efficiency into P->res_d[0..S] and the index
+// planes into P->idx (row-major, S frames). a.frame_rng holds the S streams.
+int wl_ospr_run(cgh_plan* P, const PassArgs<float>& a, int S_frames) {
+    WlState* S = wl_state(P);
+    if (!S) {
+        S = new WlState();
+        P->wlst = S;
+    }
+    const long long n = (long long)wl::N * wl::N;
+    CGH_TRY(ensure(P, S->t4, size_t(n) * 8));
+    CGH_TRY(ensure(P, S->bar, 64));
+    if (S->o_tgt_src != P->tgt.p || !S->o_tgt.p) {
+        CGH_TRY(ensure(P, S->o_tgt, size_t(n) * 4));
+        wl::perm_table_kernel<<<grid_for(n), 256, 0, P->st>>>(static_cast<const float*>(P->tgt.p),
+                                                             static_cast<float*>(S->o_tgt.p), 1.0f, 0);
+        P->launches += 1;
+        CGH_CUDA(cudaGetLastError());
+        S->o_tgt_src = P->tgt.p;
+        S->o_beam_ready = false;
+    }
+    if (P->has_beam && !S->o_beam_ready) {
+        CGH_TRY(ensure(P, S->o_beam, size_t(n) * 4));
+        wl::perm_table_kernel<<<grid_for(n), 256, 0, P->st>>>(static_cast<const float*>(P->beam.p),
+                                                             static_cast<float*>(S->o_beam.p), 1.0f, 1);
+        P->launches += 1;
+        CGH_CUDA(cudaGetLastError());
+        S->o_beam_ready = true;
+    }
+    CGH_TRY(ensure(P, S->o_states, sizeof(Pcg64) * size_t(S_frames) * wl::N));
+    CGH_TRY(ensure(P, S->o_inten, size_t(n) * 4));
+    CGH_TRY(ensure(P, S->o_idx, size_t(n) * S_frames));
+    CGH_TRY(ensure(P, S->o_sums, sizeof(double) * (size_t(S_frames) * wl::N * 3 + size_t(wl::N) * 2)));
+    const int lines = S_frames * wl::N;
+    wl::ospr_line_states_kernel<<<(lines + 255) / 256, 256, 0, P->st>>>(a.frame_rng, S_frames,
+                                                                       static_cast<Pcg64*>(S->o_states.p));
+    P->launches += 1;
+    CGH_CUDA(cudaGetLastError());
+    CGH_CUDA(cudaMemsetAsync(S->bar.p, 0, 4, P->st));
+    wl::OsprArgs o;
+    o.data = static_cast<float2*>(S->t4.p);
+    o.tgt_row = static_cast<const float*>(S->o_tgt.p);
+    o.beam_col = P->has_beam ? static_cast<const float*>(S->o_beam.p) : nullptr;
+    o.line_state = static_cast<const Pcg64*>(S->o_states.p);
+    o.inten = static_cast<float*>(S->o_inten.p);
+    o.idx_perm = static_cast<uint8_t*>(S->o_idx.p);
+    o.sums = static_cast<double*>(S->o_sums.p);
+    o.tw = a.tw_row;
+    o.q_row = a.q_row;
+    o.q_col = a.q_col;
+    o.scheme = a.scheme;
+    o.binary = (P->scheme_kind == CGH_SCHEME_PHASE && P->nstates == 2 && P->offset == 0.0) ? 1 : 0;
+    o.scale = a.scale;
+    o.S = S_frames;
+    // LCG jumps (host-computed, as jump_of): by 256, by 2, and by every first column
+    auto host_jump = [](uint64_t k) {
+        wl::Jump j;
+        u128 acc_m = 1, acc_g = 0, cur_m = pcg_mult(), cur_g = 1;
+        while (k) {
+            if (k & 1) {
+                acc_g = acc_g * cur_m + cur_g;
+                acc_m *= cur_m;
+            }
+            cur_g = (cur_m + 1) * cur_g;
+            cur_m *= cur_m;
+            k >>= 1;
+        }
+        j.A = acc_m;
+        j.G = acc_g;
+        return j;
+    };
+    if (!S->o_jumps.p) {
+        std::vector<wl::Jump> jt(wl::kJumps);
+        for (int c = 0; c < wl::kJumps; ++c) jt[c] = host_jump(uint64_t(c));
+        CGH_TRY(ensure(P, S->o_jumps, sizeof(wl::Jump) * jt.size()));
+        CGH_CUDA(cudaMemcpyAsync(S->o_jumps.p, jt.data(), sizeof(wl::Jump) * jt.size(), cudaMemcpyHostToDevice, P->st));
+        CGH_CUDA(cudaStreamSynchronize(P->st));   // jt is a temporary
+    }
+    o.jumps = static_cast<const wl::Jump*>(S->o_jumps.p);
+    o.j256 = host_jump(256);
+    o.j2 = host_jump(2);
+    if (cudaError_t e = ensure_smem_attr<wl::ospr_loop>(wl::SMEM); e != cudaSuccess)
+        return fail(CGH_ERR_CUDA, "warp-line OSPR: %s", cudaGetErrorString(e));
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, P->dev);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(std::max(1, sms));
+    cfg.blockDim = dim3(wl::THREADS);
+    cfg.dynamicSmemBytes = wl::SMEM;
+    cfg.stream = P->st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (P->profiling) CGH_TRY(prof_mark(P, 22, true));
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, wl::ospr_loop, o, static_cast<unsigned*>(S->bar.p));
+    if (P->profiling) CGH_TRY(prof_mark(P, 22, false));
+    P->launches += 1;
+    if (e != cudaSuccess) return fail(CGH_ERR_CUDA, "warp-line OSPR loop: %s", cudaGetErrorString(e));
+    wl::ospr_trace_kernel<<<std::min(S_frames + 1, 148), 96, 0, P->st>>>(o.sums, S_frames, a.red.denom,
+                                                                        P->rescale ? 1 : 0, P->res_d);
+    wl::ospr_idx_kernel<<<4 * sms, 256, 0, P->st>>>(o.idx_perm, static_cast<uint8_t*>(P->idx.p), S_frames);
+    P->launches += 2;
     CGH_CUDA(cudaGetLastError());
     return CGH_OK;
 }

@@ -16,7 +16,7 @@ from .slm import problem_for
 
 # pass ids reported by cgh_plan_profile
 PASS_NAMES = {0: "row_fwd", 1: "row_inv", 2: "row_holo", 3: "row_init", 4: "ospr_gen", 5: "ospr_acc",
-              8: "col_fwd", 9: "col_inv", 10: "col_gs", 11: "col_final", 12: "col_holo", 23: "gs_loop"}
+              8: "col_fwd", 9: "col_inv", 10: "col_gs", 11: "col_final", 12: "col_holo", 22: "ospr_loop", 23: "gs_loop"}
 
 
 def plan_key(cfg, shape, precision, device):
