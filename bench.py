@@ -395,7 +395,7 @@ def run_ours(args):
             A.run_gs(cfg, target)       # warm
             barrier()
             t0 = time.perf_counter()
-            ke = max(1, min(args.steps, 3))
+            ke = max(1, min(args.steps, 10))
             for _ in range(ke):
                 A.run_gs(cfg, target)
             barrier()

@@ -539,8 +539,10 @@ static int prep_target_host_f32(cgh_plan* P, const double* target, const uint8_t
     P->nf_beam = tot[4];
     // the denominator is read on the device (ReduceArgs::denom -> stats[1])
     double dev_stats[5] = {tot[0], tot[1], tot[2], tot[3], tot[4]};
+    // pageable source: the runtime stages it before returning (no stream sync
+    // needed for the temporary), so the last amplitude DMAs overlap the
+    // caller's next steps
     CGH_CUDA(cudaMemcpyAsync(P->stats.p, dev_stats, sizeof(dev_stats), cudaMemcpyHostToDevice, P->st));
-    CGH_CUDA(cudaStreamSynchronize(P->st));   // dev_stats is a temporary
     P->target_ready = true;
     P->stage_valid = false;
     fast_invalidate_target(P);
