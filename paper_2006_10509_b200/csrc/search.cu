@@ -79,7 +79,7 @@ struct Bcast {
 // pixel, raw level draw, stream state after the draws, prefetched index.
 struct Draw {
     Pcg64 g;
-    int m, n, jraw, idx;
+    int m, n, jraw;
 };
 
 __device__ __forceinline__ void draw_ahead(const SearchArgs& a, Pcg64 g, Draw& d) {
@@ -88,7 +88,6 @@ __device__ __forceinline__ void draw_ahead(const SearchArgs& a, Pcg64 g, Draw& d
     d.n = a.pow2 ? int(p & (a.W - 1)) : int(p % uint32_t(a.W));
     d.jraw = int(pcg_integers(g, uint64_t(a.L - 1)));
     d.g = g;
-    d.idx = read_index(a, (long long)d.m * a.W + d.n);   // consumed after the grid barrier
 }
 
 __device__ __forceinline__ double2 level_delta_s(const SearchArgs& a, const double2* st_s, int m, int n, int j, int cur) {
@@ -96,6 +95,53 @@ __device__ __forceinline__ double2 level_delta_s(const SearchArgs& a, const doub
     double2 d = make_double2(sj.x - sc.x, sj.y - sc.y);
     if (a.qr) d = dmul(d, dmul(a.qr[m], a.qc[n]));
     return d;
+}
+
+// One SA sweep on a full-mask power-of-two plane (a.colp = COLP): thread
+// tid's elements li = tid + 512 r lie in columns (begin + tid + 512 r) mod W,
+// which repeat with period COLP, so the column twiddles ct[n mv mod W] of the
+// proposal (and pending) pixel are gathered once per sweep into registers —
+// in shared memory those gathers conflict up to 8-way for even n. The row
+// twiddle rt[m mu mod H] is one address per warp (broadcast). Terms and their
+// order are those of the generic sweep (same products, same accumulation).
+template <int COLP>
+__device__ __forceinline__ double sa_sweep_cols(const SearchArgs& a, const Slice& s, const SmemLayout& L, int m,
+                                                int n, double2 d, bool pend, int pm, int pn, double2 pd) {
+    // resident slices only: L.R / L.t derive from the shared array, so the
+    // accesses compile to LDS/STS instead of generic loads
+    double2* const Rs = L.R;
+    const double* const ts = L.t;
+    const int tid = threadIdx.x, Hm = a.H - 1, Wm = a.W - 1;
+    double2 cw[COLP], cp[COLP];
+#pragma unroll
+    for (int p = 0; p < COLP; ++p) {
+        const int mv = int((s.begin + tid + (long long)kSearchThreads * p) & Wm);
+        cw[p] = L.ct[(n * mv) & Wm];
+        cp[p] = pend ? L.ct[(pn * mv) & Wm] : make_double2(0.0, 0.0);
+    }
+    double acc = 0.0;
+    for (long long li = tid; li < s.count; li += (long long)COLP * kSearchThreads) {
+#pragma unroll
+        for (int p = 0; p < COLP; ++p) {
+            const long long l = li + (long long)kSearchThreads * p;
+            if (COLP == 1 || l < s.count) {
+                const int mu = int((s.begin + l) >> a.logW);
+                double2 R = Rs[l];
+                if (pend) {
+                    const double2 u = dmul(pd, dmul(L.rt[(pm * mu) & Hm], cp[p]));
+                    R.x += u.x;
+                    R.y += u.y;
+                    Rs[l] = R;
+                }
+                const double2 u = dmul(d, dmul(L.rt[(m * mu) & Hm], cw[p]));
+                const double2 R1 = make_double2(R.x + u.x, R.y + u.y);
+                const double t = ts[l];
+                const double d0 = dabs(R) - t, d1 = dabs(R1) - t;
+                acc += d1 * d1 - d0 * d0;
+            }
+        }
+    }
+    return acc;
 }
 
 // P2: both sides powers of two (table indices by mask, not modulo)
@@ -113,13 +159,42 @@ __global__ void __launch_bounds__(kSearchThreads, 1) sa_kernel(SearchArgs a) {
     __syncthreads();
     unsigned long long phase = st.bar / gridDim.x;
     const bool lead = (blockIdx.x == 0 && threadIdx.x == 0);
-    // thread 0 state: the next proposal for both outcomes of the Metropolis draw
-    Draw nxA, nxB;
-    Pcg64 g_after_u;
-    double u_next = 0.0;
-    bool have_next = false;
-    int c1_m = -1, c1_n = -1, c1_j = 0;   // commit of the previous proposal (may not be visible yet)
+    // thread 0 state (shared memory: keeps the sweep's registers free): the
+    // next proposal for both outcomes of the Metropolis draw
+    __shared__ Draw nxA, nxB;
+    __shared__ Pcg64 g_after_u;
+    __shared__ double u_next;
+    __shared__ int have_next, c1_m, c1_n, c1_j;   // c1: commit of the previous proposal (may not be visible yet)
+    if (threadIdx.x == 0) {
+        u_next = 0.0;
+        have_next = 0;
+        c1_m = -1;
+        c1_n = -1;
+        c1_j = 0;
+    }
+    // prefetched index of the drawn pixels; trace entries written so far; proposals
+    // to the next checkpoint (thread 0 / the drawing thread 32 only)
+    __shared__ int idxA, idxB;
+    __shared__ long long trace_n, to_check;
+    if (threadIdx.x == 0) {
+        idxA = 0;
+        idxB = 0;
+        trace_n = a.write_trace ? *a.trace_len : 0;
+        to_check = a.interval - st.executed % a.interval;
+    }
+    // optional stage timing of block 0 (CGHB200_SA_PROBE): clock64 sums
+    __shared__ long long tp[8], tprev;
+    if (threadIdx.x < 8) tp[threadIdx.x] = 0;
+    const bool probe = a.probe != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
+    auto mark = [&](int k) {
+        if (probe) {
+            const long long t = clock64();
+            if (k > 0) tp[k] += t - tprev;
+            tprev = t;
+        }
+    };
     for (;;) {
+        mark(0);
         if (threadIdx.x == 0) {
             bc.pend = st.pend;
             bc.pm = st.pend_m;
@@ -130,10 +205,15 @@ __global__ void __launch_bounds__(kSearchThreads, 1) sa_kernel(SearchArgs a) {
             bc.go = warm || st.executed < a.k_end;
             if (bc.go) {
                 Draw cur_d;
-                if (!have_next) draw_ahead(a, st.rng, cur_d);
-                else cur_d = nxA;   // branch chosen at the last decision is stored in nxA
+                int cur;
+                if (!have_next) {
+                    draw_ahead(a, st.rng, cur_d);
+                    cur = read_index(a, (long long)cur_d.m * a.W + cur_d.n);
+                } else {
+                    cur_d = nxA;   // branch chosen at the last decision is stored in nxA
+                    cur = idxA;
+                }
                 st.rng = cur_d.g;
-                int cur = cur_d.idx;
                 if (st.pend && st.pend_m == cur_d.m && st.pend_n == cur_d.n) cur = st.pend_j;   // commit k-1
                 else if (c1_m == cur_d.m && c1_n == cur_d.n) cur = c1_j;                      // commit k-2
                 int j = cur_d.jraw;
@@ -148,38 +228,57 @@ __global__ void __launch_bounds__(kSearchThreads, 1) sa_kernel(SearchArgs a) {
             }
         }
         __syncthreads();
+        mark(1);
         if (!bc.go) break;
-        if (threadIdx.x == 0) {
-            // draw proposal k+1 for both outcomes while the sweep and barrier run
-            draw_ahead(a, st.rng, nxA);
-            Pcg64 gb = st.rng;
-            u_next = pcg_next_double(gb);
-            g_after_u = gb;
-            draw_ahead(a, gb, nxB);
-            have_next = true;
-        }
+        mark(2);
         const int m = bc.m, n = bc.n, pm = bc.pm, pn = bc.pn;
         const double2 d = make_double2(bc.dre, bc.dim), pd = make_double2(bc.pre, bc.pim);
         const bool pend = bc.pend != 0;
         double acc[1] = {0.0};
-        for (long long li = threadIdx.x; li < s.count; li += blockDim.x) {
-            int mu, mv;
-            element_pos(a, s, li, mu, mv);
-            double2 R = s.R[li];
-            if (pend) {
-                const double2 u = dmul(pd, tw_of<P2>(L.rt, L.ct, a, pm, pn, mu, mv));
-                R.x += u.x;
-                R.y += u.y;
-                s.R[li] = R;
+        if (P2 && a.resident && a.colp == 1) acc[0] = sa_sweep_cols<1>(a, s, L, m, n, d, pend, pm, pn, pd);
+        else if (P2 && a.resident && a.colp == 2) acc[0] = sa_sweep_cols<2>(a, s, L, m, n, d, pend, pm, pn, pd);
+        else
+            for (long long li = threadIdx.x; li < s.count; li += blockDim.x) {
+                int mu, mv;
+                element_pos(a, s, li, mu, mv);
+                double2 R = s.R[li];
+                if (pend) {
+                    const double2 u = dmul(pd, tw_of<P2>(L.rt, L.ct, a, pm, pn, mu, mv));
+                    R.x += u.x;
+                    R.y += u.y;
+                    s.R[li] = R;
+                }
+                const double2 u = dmul(d, tw_of<P2>(L.rt, L.ct, a, m, n, mu, mv));
+                const double2 R1 = make_double2(R.x + u.x, R.y + u.y);
+                const double t = s.t[li];
+                const double d0 = dabs(R) - t, d1 = dabs(R1) - t;
+                acc[0] += d1 * d1 - d0 * d0;
             }
-            const double2 u = dmul(d, tw_of<P2>(L.rt, L.ct, a, m, n, mu, mv));
-            const double2 R1 = make_double2(R.x + u.x, R.y + u.y);
-            const double t = s.t[li];
-            const double d0 = dabs(R) - t, d1 = dabs(R1) - t;
-            acc[0] += d1 * d1 - d0 * d0;
-        }
+        mark(3);
         block_sum_bcast<1>(acc, L.scratch);
-        grid_reduce(a, acc, 1, phase, red);
+        mark(4);
+        {
+            const unsigned long long* buf = grid_publish(a, acc, 1, phase);
+            if (threadIdx.x == 32) {
+                // draw proposal k+1 for both outcomes of the Metropolis draw while
+                // warp 0 waits for the other CTAs' partials
+                Draw dA, dB;
+                draw_ahead(a, st.rng, dA);
+                const int iA = read_index(a, (long long)dA.m * a.W + dA.n);
+                Pcg64 gb = st.rng;
+                u_next = pcg_next_double(gb);
+                g_after_u = gb;
+                draw_ahead(a, gb, dB);
+                const int iB = read_index(a, (long long)dB.m * a.W + dB.n);
+                nxA = dA;
+                nxB = dB;
+                idxA = iA;
+                idxB = iB;
+                have_next = 1;
+            }
+            grid_collect(buf, 1, phase, red);
+        }
+        mark(5);
         if (threadIdx.x == 0) {
             const double change = red[0];
             // the commit applied in this sweep (k-1) becomes "k-2" for the next draw
@@ -211,7 +310,8 @@ __global__ void __launch_bounds__(kSearchThreads, 1) sa_kernel(SearchArgs a) {
                     st.pend_j = bc.j;
                     st.pend_re = bc.dre;
                     st.pend_im = bc.dim;
-                    if (blockIdx.x == 0) write_index(a, (long long)bc.m * a.W + bc.n, bc.j);
+                    // every CTA writes the commit: its own later reads then see it
+                    write_index(a, (long long)bc.m * a.W + bc.n, bc.j);
                 }
                 if (lead && st.executed < a.log_cap) {
                     a.log_pixel[st.executed] = (long long)bc.m * a.W + bc.n;
@@ -220,21 +320,29 @@ __global__ void __launch_bounds__(kSearchThreads, 1) sa_kernel(SearchArgs a) {
                 }
                 st.temperature *= a.alpha;
                 st.executed += 1;
-                if (a.write_trace && (st.executed % a.interval) == 0 && lead) {
-                    const long long c = *a.trace_len;
-                    a.trace[c] = st.error_num / a.denom;
-                    a.trace_k[c] = st.executed;
-                    *a.trace_len = c + 1;
+                if (--to_check == 0) {
+                    to_check = a.interval;
+                    if (a.write_trace && lead) {
+                        const long long c = trace_n++;
+                        a.trace[c] = st.error_num / a.denom;
+                        a.trace_k[c] = st.executed;
+                        *a.trace_len = c + 1;
+                    }
                 }
             }
             if (drew) {
                 st.rng = g_after_u;   // the Metropolis draw is consumed
                 nxA = nxB;            // and the next proposal follows it
+                idxA = idxB;
             }
             // st.rng is replaced by the chosen draw's stream state at the top
         }
         __syncthreads();
+        mark(6);
+        if (probe) tp[7] += 1;
     }
+    if (probe)
+        for (int k = 1; k < 8; ++k) a.probe[k] += tp[k];
     // the stream state to persist: proposals drawn ahead are not consumed
     // (st.rng holds the state after the last consumed draws)
     if (st.pend) {
@@ -737,7 +845,11 @@ static int search_setup(SearchRun& S, int init_mode, const cgh_pcg64& rng0, bool
     if (S.smem + static_smem > size_t(optin))
         return fail(CGH_ERR_UNSUPPORTED, "search tables for %dx%d exceed shared memory", P->H, P->W);
     S.grid = std::max(1, (int)std::min<long long>(sms, std::max<long long>(S.M, 1)));
-    CGH_TRY(search_alloc(S, sizeof(double) * 2 * S.grid * kMaxWindow * kMaxLevels, reinterpret_cast<void**>(&S.partials)));
+    // phase-flagged partials (search_kernels.cuh grid_reduce): 16 B per value,
+    // two parities, zeroed so no stale flag matches a phase of this run
+    const size_t pbytes = size_t(16) * 2 * S.grid * kMaxWindow * kMaxLevels;
+    CGH_TRY(search_alloc(S, pbytes, reinterpret_cast<void**>(&S.partials)));
+    CGH_CUDA(cudaMemsetAsync(S.partials, 0, pbytes, P->st));
     return CGH_OK;
 }
 
@@ -807,6 +919,7 @@ static SearchArgs search_args(SearchRun& S) {
     a.partials = S.partials;
     a.resident = S.resident;
     a.denom = P->denom;
+    if (a.pow2 && a.full && P->W <= 1024) a.colp = std::max(1, P->W / kSearchThreads);
     return a;
 }
 
@@ -933,6 +1046,12 @@ static int sa_exec(cgh_plan* P, const cgh_sa_params* sp, int64_t* tk, double* tv
     a.trace_k = reinterpret_cast<long long*>(P->res_d + (proposals / interval + 4));
     a.trace_len = reinterpret_cast<long long*>(P->res_d + 2 * (proposals / interval + 4) + 2);
     a.write_trace = chunked ? 0 : 1;
+    long long* dprobe = nullptr;
+    if (getenv("CGHB200_SA_PROBE")) {
+        CGH_TRY(search_alloc(S, sizeof(long long) * 8, reinterpret_cast<void**>(&dprobe)));
+        CGH_CUDA(cudaMemsetAsync(dprobe, 0, sizeof(long long) * 8, P->st));
+        a.probe = dprobe;
+    }
     // decision log buffers
     long long* dlog_p = nullptr;
     int* dlog_l = nullptr;
@@ -996,6 +1115,16 @@ static int sa_exec(cgh_plan* P, const cgh_sa_params* sp, int64_t* tk, double* tv
         CGH_CUDA(cudaMemcpyAsync(sp->log_accept, dlog_a, lcap, cudaMemcpyDeviceToHost, P->st));
     }
     if (dlog_p) CGH_CUDA(cudaFreeAsync(dlog_p, P->st));
+    if (dprobe) {
+        long long hp[8];
+        CGH_CUDA(cudaMemcpyAsync(hp, dprobe, sizeof(hp), cudaMemcpyDeviceToHost, P->st));
+        CGH_CUDA(cudaStreamSynchronize(P->st));
+        const double it = hp[7] > 0 ? double(hp[7]) : 1.0;
+        fprintf(stderr, "[sa probe] %lld sweeps, cycles per sweep: top %.0f draw %.0f sweep %.0f block-sum %.0f "
+                "grid-reduce %.0f decide %.0f\n", hp[7], hp[1] / it, hp[2] / it, hp[3] / it, hp[4] / it, hp[5] / it,
+                hp[6] / it);
+        CGH_CUDA(cudaFreeAsync(dprobe, P->st));
+    }
     CGH_CUDA(cudaEventRecord(P->ev1, P->st));
     CGH_CUDA(cudaEventSynchronize(P->ev1));
     float ms = 0;

@@ -49,7 +49,7 @@ struct SearchArgs {
     void* idx;                   // index plane (H*W), idx_bytes
     int idx_bytes;
     SearchState* st;
-    double* partials;            // [2][G][NQ]
+    double* partials;            // [2][G][NQ] phase-flagged 16-B slots (grid_reduce)
     int resident;                // slices in shared memory
     double denom;
     // SA
@@ -64,6 +64,10 @@ struct SearchArgs {
     const long long* order;      // pass permutation or nullptr (raster)
     long long p_end;             // visits in this pass
     int wmax;
+    // full-mask power-of-two planes with W <= 1024: a thread's columns repeat
+    // with period colp = max(1, W / kSearchThreads) (0: generic sweep)
+    int colp;
+    long long* probe;            // SA stage clock sums of block 0 (diagnostics) or nullptr
     // decision log
     long long log_cap;
     long long* log_pixel;
@@ -133,24 +137,86 @@ __device__ __forceinline__ void block_sum_bcast(double (&v)[NQ], double* sh) {
 }
 
 // Publish per-CTA partials [nq], grid barrier, sum over CTAs in fixed order.
-__device__ __forceinline__ void grid_reduce(const SearchArgs& a, double* vals, int nq, unsigned long long& phase,
-                                            double* sh_out) {
-    const int G = gridDim.x;
-    double* buf = a.partials + (phase & 1ull) * (size_t)G * nq;
-    if (threadIdx.x < nq) buf[(size_t)blockIdx.x * nq + threadIdx.x] = vals[threadIdx.x];
+//
+// The barrier is carried by the partials themselves: a value is stored as two
+// 64-bit words (low half | phase << 32, high half | phase << 32). Aligned
+// 64-bit stores are single-copy atomic, so a reader that sees the phase in
+// both words holds the value: no counter atomics and no fences. Slots
+// alternate by phase parity (a CTA cannot run two phases ahead of a reader: it
+// needs that reader's next partial first). The buffer is zeroed per run and
+// phases start at 1. Nothing else crosses CTAs inside a launch: SA commits are
+// written to the index plane by every CTA (identical values), so each CTA
+// reads back its own writes; DBS never re-reads a pixel it committed within a
+// pass (one launch).
+constexpr int kMaxSlotsPerLane = 8;   // G <= 256 CTAs
+
+__device__ __forceinline__ void publish_slot(unsigned long long* p, double v, unsigned ph) {
+    const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(v));
+    const unsigned long long w0 = (bits & 0xffffffffull) | (static_cast<unsigned long long>(ph) << 32);
+    const unsigned long long w1 = (bits >> 32) | (static_cast<unsigned long long>(ph) << 32);
+    asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(w0), "l"(w1) : "memory");
+}
+
+__device__ __forceinline__ void load_slot(const unsigned long long* p, unsigned long long& w0, unsigned long long& w1) {
+    asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(w0), "=l"(w1) : "l"(p) : "memory");
+}
+
+// First half: threads q < nq publish vals[q] (every thread holds vals, or
+// vals is shared memory written before a __syncthreads). Advances phase.
+__device__ __forceinline__ unsigned long long* grid_publish(const SearchArgs& a, const double* vals, int nq,
+                                                           unsigned long long& phase) {
+    unsigned long long* buf =
+        reinterpret_cast<unsigned long long*>(a.partials) + ((phase & 1ull) * (size_t)gridDim.x * nq) * 2;
     phase += 1;
-    grid_sync(&a.st->bar, phase * (unsigned long long)G);
-    // warp w reduces quantities q = w, w + nwarps, ...: lane l sums CTAs
-    // l, l+32, ... (independent loads), then a fixed shuffle tree
+    if (threadIdx.x < nq) publish_slot(buf + ((size_t)blockIdx.x * nq + threadIdx.x) * 2, vals[threadIdx.x], unsigned(phase));
+    return buf;
+}
+
+// Second half: warp w reduces quantities q = w, w + nwarps, ...: lane l polls
+// CTAs l, l+32, ... together, sums them in that order, then a fixed shuffle
+// tree; totals in sh_out[q]. Ends with __syncthreads.
+__device__ __forceinline__ void grid_collect(const unsigned long long* buf, int nq, unsigned long long phase,
+                                             double* sh_out) {
+    const int G = gridDim.x;
+    const unsigned ph = unsigned(phase);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     for (int q = warp; q < nq; q += nw) {
+        double v[kMaxSlotsPerLane];
+        unsigned need = 0;
+#pragma unroll
+        for (int i = 0; i < kMaxSlotsPerLane; ++i)
+            if (lane + 32 * i < G) need |= 1u << i;
+        // one slot at a time, volatile (.SYS) accesses: measured on B200 at the
+        // C4 SA sweep (block 0 clock64, CGHB200_SA_PROBE), the barrier costs
+        // ~5.4k cycles this way, ~7.9k polling every slot per round (all loads
+        // in flight: 148 x 148 requests per round on the same L2 lines) and
+        // ~9.4k with relaxed.gpu accesses; the fenced counter barrier it
+        // replaces cost about the same as this one
+#pragma unroll
+        for (int i = 0; i < kMaxSlotsPerLane; ++i)
+            if (need & (1u << i)) {
+                const unsigned long long* p = buf + ((size_t)(lane + 32 * i) * nq + q) * 2;
+                unsigned long long w0, w1;
+                do {
+                    load_slot(p, w0, w1);
+                } while (unsigned(w0 >> 32) != ph || unsigned(w1 >> 32) != ph);
+                v[i] = __longlong_as_double(static_cast<long long>((w0 & 0xffffffffull) | (w1 << 32)));
+            }
         double s = 0;
-        for (int b = lane; b < G; b += 32) s += __ldcg(&buf[(size_t)b * nq + q]);
+#pragma unroll
+        for (int i = 0; i < kMaxSlotsPerLane; ++i)
+            if (lane + 32 * i < G) s += v[i];
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
         if (lane == 0) sh_out[q] = s;
     }
     __syncthreads();
+}
+
+__device__ __forceinline__ void grid_reduce(const SearchArgs& a, const double* vals, int nq,
+                                            unsigned long long& phase, double* sh_out) {
+    const unsigned long long* buf = grid_publish(a, vals, nq, phase);
+    grid_collect(buf, nq, phase, sh_out);
 }
 
 struct Slice {
