@@ -11,7 +11,8 @@
 // are fully unrolled with compile-time roots of unity; inter-stage twiddles
 // come from an N-entry table tw[k] = exp(-2 pi i k / N) built in fp64 on the
 // host (conjugated for the inverse). Stages exchange through shared memory
-// stored as split re/im arrays with one pad word per 128 bytes.
+// stored as split re/im arrays with one pad word per 128 bytes (complex64) or
+// as padded interleaved double2 (complex128).
 #pragma once
 #include <type_traits>
 #include "cx.cuh"
@@ -148,13 +149,20 @@ struct LineShape {
     static constexpr int TF = N / E;   // threads per line
 };
 
-// Shared-memory words per line (split re/im, padded).
+// Shared-memory words per line (split re/im, padded). complex128 lines are
+// exchanged as interleaved double2 (one 16-B access per element, half the
+// shared-memory instructions of split 8-B re/im words) with one pad element
+// per 8 (128 B): the same 2 * line_words doubles hold either layout.
 template <class T>
-__host__ __device__ constexpr int pad_unit() { return 128 / int(sizeof(T)); }
+__host__ __device__ constexpr int pad_unit() { return sizeof(T) == 8 ? 8 : 128 / int(sizeof(T)); }
+__device__ __forceinline__ int padc2(int i) { return i + (i >> 3); }
 template <class T>
 __device__ __forceinline__ int padx(int i) { return i + i / pad_unit<T>(); }
+// (complex128: the +4 makes a line's double2 region span 4 mod 8 16-B slots,
+// so the lanes of two lines interleaved in one warp (column passes) fall in
+// opposite halves of the banks)
 template <class T, int N>
-__host__ __device__ constexpr int line_words() { return N + N / pad_unit<T>() + 1; }
+__host__ __device__ constexpr int line_words() { return N + N / pad_unit<T>() + (sizeof(T) == 8 ? 4 : 1); }
 
 template <class T, int N, int DIR, int EE = LineShape<T, N>::E>
 struct LineFft {
@@ -214,9 +222,14 @@ struct LineFft {
                 const int base = (j / NS) * NS * R + (j & (NS - 1));
 #pragma unroll
                 for (int r = 0; r < R; ++r) {
-                    const int p = padx<T>(base + r * NS);
-                    sre[p] = v[b * R + r].x;
-                    sim[p] = v[b * R + r].y;
+                    if constexpr (sizeof(T) == 8) {
+                        reinterpret_cast<double2*>(sre)[padc2(base + r * NS)] =
+                            make_double2(v[b * R + r].x, v[b * R + r].y);
+                    } else {
+                        const int p = padx<T>(base + r * NS);
+                        sre[p] = v[b * R + r].x;
+                        sim[p] = v[b * R + r].y;
+                    }
                 }
             }
             __syncthreads();
@@ -226,8 +239,13 @@ struct LineFft {
             for (int b = 0; b < NB2; ++b)
 #pragma unroll
                 for (int r = 0; r < R2; ++r) {
-                    const int p = padx<T>(t + b * TF + r * (N / R2));
-                    v[b * R2 + r] = mk(sre[p], sim[p]);
+                    if constexpr (sizeof(T) == 8) {
+                        const double2 z = reinterpret_cast<const double2*>(sre)[padc2(t + b * TF + r * (N / R2))];
+                        v[b * R2 + r] = mk<T>(z.x, z.y);
+                    } else {
+                        const int p = padx<T>(t + b * TF + r * (N / R2));
+                        v[b * R2 + r] = mk(sre[p], sim[p]);
+                    }
                 }
             stages<NS * R>(v, sre, sim, t, tw);
         }
