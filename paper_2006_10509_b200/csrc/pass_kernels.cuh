@@ -333,6 +333,10 @@ struct LaunchShape {
     }
     static int col_cols(int W) {
         // 512 threads per CTA: C columns side by side across lanes
+        // (CGH_FP64_COLS overrides it for complex128 lines, A/B builds)
+#ifdef CGH_FP64_COLS
+        if (sizeof(T) == 8 && N >= 1024) return CGH_FP64_COLS;
+#endif
         return TF >= 512 ? 1 : 512 / TF;
     }
 };
