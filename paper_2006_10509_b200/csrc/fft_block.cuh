@@ -142,6 +142,7 @@ __device__ __forceinline__ cx<T> tw_at(const TwSplit<T>& s, int k) {
 }
 
 // Elements per thread for a line of N points at precision T.
+// (complex128 at 4 points per thread, 512-thread lines: C3 fp64 74 vs 53 ms)
 template <class T, int N>
 struct LineShape {
     static constexpr int EMAX = sizeof(T) == 8 ? 8 : 16;

@@ -32,8 +32,16 @@ __device__ __forceinline__ cx<T> unit_phase(Pcg64& g) {
 // ============================================================== row kernel
 // Launch bound = the CTA size launch_row_n uses (max(TF, 256) threads: one
 // 4096-point complex128 line takes 512 threads at 8 elements each).
+// complex128 rows at 256 threads ask ptxas for 3 resident CTAs per SM (80
+// registers; 24 warps instead of 16): C3 fp64 53.1 -> 51.2 ms per 200
+// iterations on B200. 0 = no minimum (the default bound).
+template <class T, int N>
+struct RowBounds {
+    static constexpr int THREADS = LineShape<T, N>::TF >= 256 ? LineShape<T, N>::TF : 256;
+    static constexpr int MINB = (sizeof(T) == 8 && THREADS == 256) ? 3 : 0;
+};
 template <class T, int N, int MODE>
-__global__ void __launch_bounds__(LineShape<T, N>::TF >= 256 ? LineShape<T, N>::TF : 256) row_kernel(PassArgs<T> a) {
+__global__ void __launch_bounds__(RowBounds<T, N>::THREADS, RowBounds<T, N>::MINB) row_kernel(PassArgs<T> a) {
     using Sh = LineShape<T, N>;
     constexpr int E = Sh::E, TF = Sh::TF;
     constexpr int WORDS = line_words<T, N>();
@@ -235,8 +243,13 @@ __global__ void __launch_bounds__(LineShape<T, N>::TF >= 256 ? LineShape<T, N>::
 }
 
 // =========================================================== column kernel
+// (CGH_COL_LB_THREADS / CGH_COL_LB_MINB: A/B builds of the complex128 column pass)
+#ifndef CGH_COL_LB_THREADS
+#define CGH_COL_LB_THREADS 512
+#define CGH_COL_LB_MINB 0
+#endif
 template <class T, int N, int MODE>
-__global__ void __launch_bounds__(512) col_kernel(PassArgs<T> a) {
+__global__ void __launch_bounds__(CGH_COL_LB_THREADS, CGH_COL_LB_MINB) col_kernel(PassArgs<T> a) {
     using Sh = LineShape<T, N>;
     constexpr int E = Sh::E, TF = Sh::TF;
     constexpr int WORDS = line_words<T, N>();
