@@ -259,10 +259,15 @@ template <int N, int TH, int MINB>
 static cudaError_t holo_launch_th(cgh_plan* P, const FastHoloArgs& h, const CUtensorMap& map) {
     using S = FastShape<N, TH>;
     const size_t smem = size_t(2) * ((S::LINES * S::LW + 15) / 16 * 16) * sizeof(float2);
-    auto k = fast_col_holo<N, TH, MINB>;
-    if (cudaError_t e = ensure_smem_attr<fast_col_holo<N, TH, MINB>>(smem); e != cudaSuccess) return e;
     const int tiles = h.frames * (P->W / S::LINES);
     const int grid = std::max(1, std::min(MINB * sm_count(P->dev), tiles));
+    if (h.binary && !h.beam && !h.q_row) {
+        auto k = fast_col_holo<N, TH, MINB, true>;
+        if (cudaError_t e = ensure_smem_attr<fast_col_holo<N, TH, MINB, true>>(smem); e != cudaSuccess) return e;
+        return launch_pdl(k, grid, TH, smem, P->st, h, map);
+    }
+    auto k = fast_col_holo<N, TH, MINB>;
+    if (cudaError_t e = ensure_smem_attr<fast_col_holo<N, TH, MINB>>(smem); e != cudaSuccess) return e;
     return launch_pdl(k, grid, TH, smem, P->st, h, map);
 }
 

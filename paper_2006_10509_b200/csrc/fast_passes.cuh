@@ -668,7 +668,11 @@ struct FastHoloArgs {
     unsigned* tile_ctr;
 };
 
-template <int N, int TH, int MINB>
+// PLAIN: binary scheme (PhaseOnly(2), offset 0), no illumination, Fourier
+// propagation — the beam loads, chirp products and their null checks compile
+// out, the two state values sit in registers. Same arithmetic as the general
+// path for those inputs (bitwise identical planes).
+template <int N, int TH, int MINB, bool PLAIN = false>
 __global__ void __launch_bounds__(TH, MINB) fast_col_holo(FastHoloArgs a, const __grid_constant__ CUtensorMap tmap) {
     using S = FastShape<N, TH>;
     constexpr int TF = S::TF, C = S::LINES, LW = S::LW;
@@ -710,7 +714,12 @@ __global__ void __launch_bounds__(TH, MINB) fast_col_holo(FastHoloArgs a, const 
         }
     }
     __syncthreads();
-    const bool fres = a.q_row != nullptr;
+    const bool fres = !PLAIN && a.q_row != nullptr;
+    float2 st0 = make_float2(0.0f, 0.0f), st1 = st0;
+    if constexpr (PLAIN) {
+        st0 = sst[0];
+        st1 = sst[1];
+    }
     for (int it = 0;; ++it) {
         const int s = it & 1;
         const int tile = tileq[s];
@@ -730,10 +739,30 @@ __global__ void __launch_bounds__(TH, MINB) fast_col_holo(FastHoloArgs a, const 
         }
         float2* line = buf + c * LW;
         fast_fft<N, TH, +1>(v, line, t, pt, tw);
-        const cx<float> qn = fres ? a.q_col[n] : mk(1.0f, 0.0f);
         uint8_t* ip = a.idx + size_t(f) * N * a.W + n;
+        if constexpr (PLAIN) {
+            // amp = 1: h = x / |x| (1 + 0i for x = 0); k by the sign of Re h,
+            // the reference formula when Re h == 0
 #pragma unroll
-        for (int r = 0; r < 16; ++r) {
+            for (int r = 0; r < 16; ++r) {
+                const cx<float> x = v[r];
+                const float m2 = x.x * x.x + x.y * x.y;
+                cx<float> h;
+                if (m2 > 0.0f) {
+                    const float k = rsqrtf(m2);
+                    h = mk(x.x * k, x.y * k);
+                } else {
+                    h = mk(1.0f, 0.0f);
+                }
+                const int k = h.x != 0.0f ? (h.x < 0.0f ? 1 : 0) : quantize_index<float>(a.scheme, h);
+                ip[size_t(t + r * TF) * a.W] = uint8_t(k);
+                const float2 z = k ? st1 : st0;
+                v[r] = mk(z.x, z.y);
+            }
+        }
+        const cx<float> qn = fres ? a.q_col[n] : mk(1.0f, 0.0f);
+#pragma unroll
+        for (int r = 0; r < (PLAIN ? 0 : 16); ++r) {
             const int m = t + r * TF;
             cx<float> x = v[r];
             cx<float> q = mk(1.0f, 0.0f);
