@@ -857,6 +857,16 @@ struct FastOsprArgs {
     unsigned* tile_ctr;
 };
 
+// sqrt.approx (one MUFU op, <= 2 ulp) for K3's perceived amplitudes: they
+// only enter the error / efficiency sums, whose tolerance is 1e-3 relative
+// (the IEEE sqrtf carried a slow-path branch per element: 12% of K3's stall
+// samples were branch instructions, profiles/r02_ncu_ospr_c2_full.json)
+__device__ __forceinline__ float sqrt_fast(float x) {
+    float r;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
 // K1: random-phase sub-target of row u (uncentred) -> inverse row FFT.
 template <int N, int TH, int MINB>
 __global__ void __launch_bounds__(TH, MINB) fast_ospr_gen(FastOsprArgs a) {
@@ -988,7 +998,7 @@ __global__ void __launch_bounds__(TH, MINB) fast_ospr_acc(FastOsprArgs a) {
                 const float x = v[r].x * a.scale, y = v[r].y * a.scale;
                 inten[r] += x * x + y * y;
                 const bool in = !signbit(tv[r]);
-                const float p = sqrtf(inten[r] * inv_n);
+                const float p = sqrt_fast(inten[r] * inv_n);
                 const float d = p - tv[r];
                 sdd += in ? d * d : 0.f;
                 spp += in ? p * p : 0.f;
@@ -1025,7 +1035,7 @@ __global__ void __launch_bounds__(TH, MINB) fast_ospr_acc(FastOsprArgs a) {
             float sin_ = 0.f, sall = 0.f;
 #pragma unroll
             for (int r = 0; r < 16; ++r) {
-                const float p = sqrtf(inten[r] * inv_n);
+                const float p = sqrt_fast(inten[r] * inv_n);
                 const float pp = p * p;
                 sall += pp;
                 sin_ += !signbit(tv[r]) ? pp : 0.f;

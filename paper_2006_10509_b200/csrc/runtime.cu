@@ -23,6 +23,11 @@ void set_error(const char* fmt, ...) {
     g_err = buf;
 }
 
+std::shared_mutex& device_gate(int dev) {
+    static std::shared_mutex m[64];
+    return m[dev & 63];
+}
+
 int fail(int code, const char* fmt, ...) {
     char buf[1024];
     va_list ap;
@@ -1243,6 +1248,7 @@ int cgh_plan_gs(cgh_plan* plan, const cgh_gs_params* gp, int64_t* trace_k, doubl
                 cgh_report* rep, const cgh_callbacks* cb) {
     if (!plan || !gp) return fail(CGH_ERR_VALUE, "null argument");
     CGH_CUDA(cudaSetDevice(plan->dev));
+    GateLock gate(plan->dev, wl_eligible(plan));   // the warp-line loop is a grid-barrier kernel
     return plan->prec == CGH_FP64 ? gs_exec<double>(plan, gp, trace_k, trace_v, trace_cap, rep, cb, nullptr)
                                   : gs_exec<float>(plan, gp, trace_k, trace_v, trace_cap, rep, cb, nullptr);
 }
@@ -1251,6 +1257,7 @@ int cgh_plan_ospr(cgh_plan* plan, const cgh_ospr_params* op, int64_t* trace_k, d
                   cgh_report* rep, const cgh_callbacks* cb) {
     if (!plan || !op) return fail(CGH_ERR_VALUE, "null argument");
     CGH_CUDA(cudaSetDevice(plan->dev));
+    GateLock gate(plan->dev, wl_ospr_eligible(plan));
     return plan->prec == CGH_FP64 ? ospr_exec<double>(plan, op, trace_k, trace_v, trace_cap, rep, cb)
                                   : ospr_exec<float>(plan, op, trace_k, trace_v, trace_cap, rep, cb);
 }
@@ -1259,6 +1266,7 @@ int cgh_plan_ospr_part(cgh_plan* plan, const cgh_ospr_params* op, int32_t frame0
                        int32_t phase, int64_t* trace_k, double* trace_v, int64_t trace_cap, cgh_report* rep) {
     if (!plan || !op) return fail(CGH_ERR_VALUE, "null argument");
     CGH_CUDA(cudaSetDevice(plan->dev));
+    GateLock gate(plan->dev, false);
     return plan->prec == CGH_FP64
                ? ospr_part_exec<double>(plan, op, frame0, nframes_total, phase, trace_k, trace_v, trace_cap, rep)
                : ospr_part_exec<float>(plan, op, frame0, nframes_total, phase, trace_k, trace_v, trace_cap, rep);
@@ -1460,6 +1468,7 @@ int cgh_gs_run(const cgh_problem* pb, const cgh_gs_params* gp, const double* tar
     const long n = long(P->H) * P->W;
     DevBuf& fb = P->field;
     if (out_field) CGH_TRY(ensure(P, fb, size_t(n) * (P->prec == CGH_FP64 ? 16 : 8)));
+    GateLock gate(P->dev, wl_eligible(P));
     int s = P->prec == CGH_FP64
                 ? gs_exec<double>(P, gp, trace_k, trace_v, trace_cap, rep, cb, out_field ? static_cast<cx<double>*>(fb.p) : nullptr)
                 : gs_exec<float>(P, gp, trace_k, trace_v, trace_cap, rep, cb, out_field ? static_cast<cx<float>*>(fb.p) : nullptr);

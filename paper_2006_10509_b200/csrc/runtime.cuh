@@ -7,6 +7,8 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
+#include <shared_mutex>
 #include <string>
 #include <vector>
 
@@ -18,6 +20,32 @@ namespace cgh {
 // ----------------------------------------------------------------- errors
 void set_error(const char* fmt, ...);
 int fail(int code, const char* fmt, ...);
+
+// Kernels whose CTAs wait on each other (grid barriers: the SA/DBS search
+// kernels, the warp-line loops) need every CTA resident. Launched onto one
+// device while another host thread's work is on it (run_batch workers
+// sharing a GPU), such a grid can be left partly resident behind CTAs that
+// themselves wait — another grid-barrier kernel, or kernels launched early
+// with programmatic dependent launch waiting for their predecessor — and
+// both sides wait forever (seen in the 3-thread run_batch test). Runs take
+// this per-device gate for their whole duration (every run synchronizes
+// before it returns): shared by runs that only launch ordinary kernels,
+// exclusive for runs that may launch a grid-barrier kernel.
+std::shared_mutex& device_gate(int dev);
+struct GateLock {
+    std::shared_mutex& m;
+    bool ex;
+    GateLock(int dev, bool exclusive) : m(device_gate(dev)), ex(exclusive) {
+        if (ex) m.lock();
+        else m.lock_shared();
+    }
+    ~GateLock() {
+        if (ex) m.unlock();
+        else m.unlock_shared();
+    }
+    GateLock(const GateLock&) = delete;
+    GateLock& operator=(const GateLock&) = delete;
+};
 
 #define CGH_CUDA(call)                                                                      \
     do {                                                                                    \

@@ -995,6 +995,7 @@ static int audit_call(SearchRun& S, const cgh_callbacks* cb, int64_t k, double i
 
 static int sa_exec(cgh_plan* P, const cgh_sa_params* sp, int64_t* tk, double* tv, int64_t cap, cgh_report* rep,
                    const cgh_callbacks* cb) {
+    GateLock gate(P->dev, true);   // grid-barrier kernels: the device to this run (runtime.cuh)
     if (P->prec != CGH_FP64) return fail(CGH_ERR_VALUE, "search runs need an fp64 plan");
     if (sp->init_mode != CGH_INIT_RANDOM_PHASE && sp->init_mode != CGH_INIT_BACKPROPAGATE)
         return fail(CGH_ERR_VALUE, "unknown init mode %d", sp->init_mode);
@@ -1143,6 +1144,7 @@ static int sa_exec(cgh_plan* P, const cgh_sa_params* sp, int64_t* tk, double* tv
 
 static int dbs_exec(cgh_plan* P, const cgh_dbs_params* dp, int64_t* tk, double* tv, int64_t cap, cgh_report* rep,
                     const cgh_callbacks* cb) {
+    GateLock gate(P->dev, true);   // grid-barrier kernels: the device to this run (runtime.cuh)
     if (P->prec != CGH_FP64) return fail(CGH_ERR_VALUE, "search runs need an fp64 plan");
     if (dp->init_mode != CGH_INIT_RANDOM_PHASE && dp->init_mode != CGH_INIT_BACKPROPAGATE)
         return fail(CGH_ERR_VALUE, "unknown init mode %d", dp->init_mode);
