@@ -882,7 +882,10 @@ __global__ void __launch_bounds__(TH, MINB) fast_ospr_gen(FastOsprArgs a) {
     __shared__ int lineq[8];
     FastTw<N, TH> tw;
     fast_tw_init<N, TH>(tw, t, a.tw_row);
-    const LcgJump jt = lcg_jump(uint64_t(16) * t);   // this thread's chunk offset in the row
+    // this thread's chunk of 16 draws in the row, as two chains of 8 (draws
+    // 16t.. and 16t+8..): two independent 128-bit LCG recurrences per step
+    // (the single chain was latency bound on its IMAD/IADD3 carries)
+    const LcgJump jt = lcg_jump(uint64_t(16) * t), jt8 = lcg_jump(uint64_t(16) * t + 8);
     pdl_wait();
     stagger_group(g);
     const int nlines = a.frames * a.H;
@@ -894,20 +897,33 @@ __global__ void __launch_bounds__(TH, MINB) fast_ospr_gen(FastOsprArgs a) {
         const int f = ln / a.H, u = ln - f * a.H;
         const int uc = (u + a.H / 2) % a.H;
         const Pcg64 s0 = a.line_state[f * a.H + uc];
-        Pcg64 gen;
-        gen.state = jt.A * s0.state + s0.inc * jt.G;
-        gen.inc = s0.inc;
-        gen.has_uint32 = 0;
-        gen.uinteger = 0;
-        const float* trow = a.tgt + size_t(u) * N;
-#pragma unroll 4
-        for (int e = 0; e < 16; ++e) {
-            float sn, cs;
+        Pcg64 ga, gb;
+        ga.state = jt.A * s0.state + s0.inc * jt.G;
+        gb.state = jt8.A * s0.state + s0.inc * jt8.G;
+        ga.inc = gb.inc = s0.inc;
+        ga.has_uint32 = gb.has_uint32 = 0;
+        ga.uinteger = gb.uinteger = 0;
+        // uncentred columns of centred 16t..16t+15: 16 contiguous amplitudes
+        const int p0 = (16 * t + N / 2) & (N - 1);
+        const float4* t4 = reinterpret_cast<const float4*>(a.tgt + size_t(u) * N + p0);
+        float amp[16];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const float4 z = __ldg(t4 + q);
+            amp[4 * q] = z.x;
+            amp[4 * q + 1] = z.y;
+            amp[4 * q + 2] = z.z;
+            amp[4 * q + 3] = z.w;
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            float sa, ca, sb, cb;
             // angle / pi in [-1, 1); SFU sine / cosine (abs. error < 4e-7 on [-pi, pi])
-            __sincosf(3.14159265358979f * pcg_next_halfturns(gen), &sn, &cs);
-            const int pos = (16 * t + e + N / 2) & (N - 1);   // uncentred column of centred 16t+e
-            const float amp = fabsf(trow[pos]);
-            line[padc(pos)] = make_float2(amp * cs, amp * sn);
+            __sincosf(3.14159265358979f * pcg_next_halfturns(ga), &sa, &ca);
+            __sincosf(3.14159265358979f * pcg_next_halfturns(gb), &sb, &cb);
+            const float aa = fabsf(amp[e]), ab = fabsf(amp[e + 8]);
+            line[padc(p0 + e)] = make_float2(aa * ca, aa * sa);
+            line[padc(p0 + e + 8)] = make_float2(ab * cb, ab * sb);
         }
         group_sync(bid, TF);
         cx<float> v[16];
