@@ -518,7 +518,7 @@ __global__ void __launch_bounds__(kSearchThreads, 1) dbs_kernel(SearchArgs a) {
             part[q] = v;
         }
         __syncthreads();
-        grid_reduce(a, part, NQ, phase, red);
+        grid_reduce_counter(a, part, NQ, phase, red);
         if (threadIdx.x == 0) {
             st.pend = 0;
             int advanced = W;

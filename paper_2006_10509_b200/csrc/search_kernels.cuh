@@ -144,10 +144,9 @@ __device__ __forceinline__ void block_sum_bcast(double (&v)[NQ], double* sh) {
 // both words holds the value: no counter atomics and no fences. Slots
 // alternate by phase parity (a CTA cannot run two phases ahead of a reader: it
 // needs that reader's next partial first). The buffer is zeroed per run and
-// phases start at 1. Nothing else crosses CTAs inside a launch: SA commits are
-// written to the index plane by every CTA (identical values), so each CTA
-// reads back its own writes; DBS never re-reads a pixel it committed within a
-// pass (one launch).
+// phases start at 1. Nothing else crosses CTAs inside an SA launch: commits
+// are written to the index plane by every CTA (identical values), so each CTA
+// reads back its own writes. (SA only; DBS uses grid_reduce_counter below.)
 constexpr int kMaxSlotsPerLane = 8;   // G <= 256 CTAs
 
 __device__ __forceinline__ void publish_slot(unsigned long long* p, double v, unsigned ph) {
@@ -219,6 +218,29 @@ __device__ __forceinline__ void grid_reduce(const SearchArgs& a, const double* v
                                             unsigned long long& phase, double* sh_out) {
     const unsigned long long* buf = grid_publish(a, vals, nq, phase);
     grid_collect(buf, nq, phase, sh_out);
+}
+
+// DBS keeps the fenced counter barrier (grid_sync on st->bar): with the
+// phase-flagged partials above, DBS at 128^2 and 256^2 hung on B200 (64^2,
+// 512^2 and 1024^2 completed; cause not found), and DBS pays one barrier per
+// window of up to 32 pixels, so the flagged form buys it little. Partials are
+// plain doubles [2][G][nq] here.
+__device__ __forceinline__ void grid_reduce_counter(const SearchArgs& a, const double* vals, int nq,
+                                                    unsigned long long& phase, double* sh_out) {
+    const int G = gridDim.x;
+    double* buf = a.partials + (phase & 1ull) * (size_t)G * nq;
+    if (threadIdx.x < nq) buf[(size_t)blockIdx.x * nq + threadIdx.x] = vals[threadIdx.x];
+    phase += 1;
+    grid_sync(&a.st->bar, phase * (unsigned long long)G);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int q = warp; q < nq; q += nw) {
+        double s = 0;
+        for (int b = lane; b < G; b += 32) s += __ldcg(&buf[(size_t)b * nq + q]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) sh_out[q] = s;
+    }
+    __syncthreads();
 }
 
 struct Slice {
