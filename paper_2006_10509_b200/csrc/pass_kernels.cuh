@@ -35,10 +35,13 @@ __device__ __forceinline__ cx<T> unit_phase(Pcg64& g) {
 // complex128 rows at 256 threads ask ptxas for 3 resident CTAs per SM (80
 // registers; 24 warps instead of 16): C3 fp64 53.1 -> 51.2 ms per 200
 // iterations on B200. 0 = no minimum (the default bound).
+#ifndef CGH_F64_ROW_MINB
+#define CGH_F64_ROW_MINB 3
+#endif
 template <class T, int N>
 struct RowBounds {
     static constexpr int THREADS = LineShape<T, N>::TF >= 256 ? LineShape<T, N>::TF : 256;
-    static constexpr int MINB = (sizeof(T) == 8 && THREADS == 256) ? 3 : 0;
+    static constexpr int MINB = (sizeof(T) == 8 && THREADS == 256) ? CGH_F64_ROW_MINB : 0;
 };
 template <class T, int N, int MODE>
 __global__ void __launch_bounds__(RowBounds<T, N>::THREADS, RowBounds<T, N>::MINB) row_kernel(PassArgs<T> a) {
